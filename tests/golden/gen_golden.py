@@ -1,0 +1,387 @@
+"""Generate the golden fixtures from the reference implementation itself.
+
+Run in the build container (the only place ``/root/reference`` exists)::
+
+    python tests/golden/gen_golden.py
+
+It imports the read-only reference package ``lopec`` (``/root/reference/pkg/src``),
+compiles ``.lope`` programs with the reference frontend, runs them on the
+reference ``Machine`` / ``oracle_step`` in float64 and writes small fixtures:
+
+* ``kernels.json``  — every kernel's reference lowering, serialised in this
+  repo's LOPE1 text form (pins ``stencils.py`` and the IR converter);
+* ``runs.npz``      — input fields and reference outputs for K = 1/5/20 steps,
+  single image and slab-decomposed (``images=P, grid_rows=P``), plus rank-3
+  ``oracle_step`` runs;
+* ``exchange.npz``  — every padded cell of every block after one
+  ``HALO_TRANSFER`` on slab-decomposed grids (``runtime.py:643-711``);
+* ``random.npz`` + ``random.json`` — random kernels (offsets in [-2,2], + - * /,
+  abs/min/max/sqrt, scalar parameters, locals) with one ``oracle_step``;
+* ``kats.json``     — point-source / corner / fixed-point / layout KATs.
+
+Nothing here runs on the GPU box; the fixtures travel, the reference does not.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import pathlib
+import random
+import sys
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(REPO))
+sys.dont_write_bytecode = True
+
+from lopec import check_program, parse_source  # noqa: E402
+from lopec.ir import StorageLayout, lower_kernel, map_local_to_global  # noqa: E402
+from lopec.runtime import Machine, RunConfig, oracle_step  # noqa: E402
+
+from paper_1502_03504_b200.ir import from_lopec, serialize  # noqa: E402
+
+CORPUS = pathlib.Path("/root/reference/pkg/corpus")
+
+KERNEL_SRC = {
+    "heat2d": ("""\
+pure concurrent subroutine heat2d(U)
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: U
+  U(0,0) = U(0,0) + 0.125*(U(-1,0) + U(+1,0) + U(0,-1) + U(0,+1) - 4*U(0,0))
+end subroutine heat2d
+""", 2, 1),
+    "ninept2d": ("""\
+pure concurrent subroutine ninept2d(U)
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: U
+  U(0,0) = (4*U(0,0) + 2*(U(-1,0) + U(+1,0) + U(0,-1) + U(0,+1)) &
+           + U(-1,-1) + U(+1,-1) + U(-1,+1) + U(+1,+1)) / 16
+end subroutine ninept2d
+""", 2, 1),
+    "box5x5": ("""\
+pure concurrent subroutine box5x5(U)
+  real, dimension(:,:), HALO(2:*:2, 2:*:2) :: U
+  U(0,0) = (U(-2,-2) + U(-1,-2) + U(0,-2) + U(+1,-2) + U(+2,-2) &
+          + U(-2,-1) + U(-1,-1) + U(0,-1) + U(+1,-1) + U(+2,-1) &
+          + U(-2,0) + U(-1,0) + U(0,0) + U(+1,0) + U(+2,0) &
+          + U(-2,+1) + U(-1,+1) + U(0,+1) + U(+1,+1) + U(+2,+1) &
+          + U(-2,+2) + U(-1,+2) + U(0,+2) + U(+1,+2) + U(+2,+2)) / 25
+end subroutine box5x5
+""", 2, 2),
+    "lap3d7": ("""\
+pure concurrent subroutine lap3d7(U)
+  real, dimension(:,:,:), HALO(1:*:1, 1:*:1, 1:*:1) :: U
+  U(0,0,0) = U(0,0,0) + 0.125*(U(-1,0,0) + U(+1,0,0) + U(0,-1,0) + U(0,+1,0) &
+             + U(0,0,-1) + U(0,0,+1) - 6*U(0,0,0))
+end subroutine lap3d7
+""", 3, 1),
+}
+
+MAIN_2D = """\
+program main
+  real, allocatable, dimension(:,:), codimension[:,:], HALO({w}:*:{w}, {w}:*:{w}) :: U
+  integer :: device
+  integer :: it
+  device = GET_SUBIMAGE(1)
+  allocate(U({lo}:M+{w}, {lo}:N+{w})[MP,*])
+  if (device /= this_image()) then
+    allocate(U[device], HALO_SRC=U) [[device]]
+  end if
+  do it = 1, nsteps
+    call HALO_TRANSFER(U, BC=CYCLIC)
+    do concurrent (i=1:M, j=1:N) [[device]]
+      call {k}( U(i,j)[device] )
+    end do
+  end do
+  if (device /= this_image()) then
+    U = U[device]
+  end if
+end program main
+"""
+
+
+def compile_text(text, name="gen.lope"):
+    program, diags = parse_source(text, name)
+    assert program is not None and not diags, [d.render() for d in diags]
+    result = check_program(program)
+    assert result.ok, [d.render() for d in result.diagnostics]
+    return result
+
+
+def program_for(kname):
+    src, rank, w = KERNEL_SRC[kname]
+    if rank == 3:
+        return compile_text(src + "program main\nend program main\n")
+    return compile_text(src + MAIN_2D.format(w=w, lo=1 - w, k=kname))
+
+
+def run_machine(result, field, **kw):
+    m = Machine(result, RunConfig(**kw), field)
+    m.run()
+    return m
+
+
+def gen_kernels():
+    out = {}
+    for stem, kname in (("laplacian", "laplacian"), ("avg3", "avg3"), ("upwind", "drift2")):
+        r = compile_text((CORPUS / f"{stem}.lope").read_text(), f"{stem}.lope")
+        out[kname] = serialize(from_lopec(lower_kernel(r.kernels[kname])))
+    for kname in KERNEL_SRC:
+        r = program_for(kname)
+        out[kname] = serialize(from_lopec(lower_kernel(r.kernels[kname])))
+    (HERE / "kernels.json").write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
+    return out
+
+
+def gen_runs():
+    rng = np.random.default_rng(20260823)     # seed of test_acceptance.py:91
+    arrays = {}
+    index = []
+    cases = [
+        ("laplacian", CORPUS / "laplacian.lope", (8, 8), {}),
+        ("laplacian", CORPUS / "laplacian.lope", (32, 32), {}),
+        ("avg3", CORPUS / "avg3.lope", (64, 1), {}),
+        ("drift2", CORPUS / "upwind.lope", (32, 32), {"c": 0.25}),
+        ("heat2d", None, (32, 24), {}),
+        ("ninept2d", None, (24, 32), {}),
+        ("box5x5", None, (20, 16), {}),
+    ]
+    for kname, path, shape, scal in cases:
+        result = (compile_text(path.read_text(), path.name) if path is not None
+                  else program_for(kname))
+        kir = lower_kernel(result.kernels[kname])
+        for steps in (1, 5, 20):
+            field = rng.uniform(-1.0, 1.0, shape)
+            tag = f"{kname}_{shape[0]}x{shape[1]}_k{steps}"
+            base = run_machine(result, field.copy(), images=1, steps=steps).gather()
+            ref = field[:, 0] if shape[1] == 1 else field.copy()
+            for _ in range(steps):
+                ref = oracle_step(ref, kir, {k: np.float64(v) for k, v in scal.items()})
+            got = base[:, 0] if shape[1] == 1 else base
+            assert np.array_equal(ref, got), tag
+            arrays[tag + "_in"] = field[:, 0] if shape[1] == 1 else field
+            arrays[tag + "_out"] = got
+            decomp = []
+            if shape[1] > 1:
+                for p in (2, 4):
+                    if shape[1] % p == 0 and shape[1] // p >= max(1, KERNEL_SRC.get(kname, ("", 2, 2))[2]):
+                        g = run_machine(result, field.copy(), images=p, grid_rows=p,
+                                        steps=steps).gather()
+                        assert np.array_equal(g, base), (tag, p)
+                        decomp.append(p)
+            index.append({"tag": tag, "kernel": kname, "shape": list(got.shape), "steps": steps,
+                          "scalars": scal, "decomp_checked": decomp})
+    # rank 3: the reference Machine rejects rank-3 coarrays (F6); oracle_step covers it
+    result = program_for("lap3d7")
+    kir = lower_kernel(result.kernels["lap3d7"])
+    for shape, steps in (((12, 10, 8), 1), ((12, 10, 8), 5), ((9, 7, 6), 20)):
+        field = rng.uniform(-1.0, 1.0, shape)
+        ref = field.copy()
+        for _ in range(steps):
+            ref = oracle_step(ref, kir, {})
+        tag = f"lap3d7_{'x'.join(map(str, shape))}_k{steps}"
+        arrays[tag + "_in"] = field
+        arrays[tag + "_out"] = ref
+        index.append({"tag": tag, "kernel": "lap3d7", "shape": list(shape), "steps": steps,
+                      "scalars": {}, "decomp_checked": []})
+    np.savez_compressed(HERE / "runs.npz", **arrays)
+    (HERE / "runs.json").write_text(json.dumps(index, indent=1) + "\n")
+
+
+EXCHANGE_TEMPLATE = """\
+program main
+  real, allocatable, dimension(:,:), codimension[:,:], &
+        HALO({l0}:*:{h0}, {l1}:*:{h1}) :: U
+  allocate(U(1-{l0}:M+{h0}, 1-{l1}:N+{h1})[MP,*])
+  call HALO_TRANSFER(U, BC=CYCLIC)
+end program main
+"""
+
+
+def gen_exchange():
+    rng = np.random.default_rng(104)
+    arrays = {}
+    index = []
+    for widths in ((1, 1, 1, 1), (2, 2, 2, 2), (2, 0, 1, 1), (0, 2, 2, 1), (1, 2, 0, 0)):
+        result = compile_text(EXCHANGE_TEMPLATE.format(l0=widths[0], h0=widths[1],
+                                                       l1=widths[2], h1=widths[3]))
+        for p in (1, 2, 4):
+            field = rng.uniform(-1, 1, (8, 8))
+            m = run_machine(result, field.copy(), images=p, grid_rows=p)
+            tag = f"x{''.join(map(str, widths))}_p{p}"
+            arrays[tag + "_in"] = field
+            for k in m.images:
+                arrays[f"{tag}_blk{k}"] = m.arrays["u"].view(k).copy()
+            index.append({"tag": tag, "widths": list(widths), "p": p})
+    np.savez_compressed(HERE / "exchange.npz", **arrays)
+    (HERE / "exchange.json").write_text(json.dumps(index, indent=1) + "\n")
+
+
+def _rand_expr(rng, depth, rank, scalars):
+    if depth == 0 or rng.random() < 0.3:
+        kind = rng.randrange(4 if scalars else 3)
+        if kind == 0:
+            offs = [rng.randrange(-2, 3) for _ in range(rank)]
+            return "U(" + ",".join(("+" if o > 0 else "") + str(o) for o in offs) + ")"
+        if kind == 1:
+            return f"{rng.randrange(1, 5)}"
+        if kind == 2:
+            return f"{rng.uniform(0.25, 2.0):.3f}"
+        return rng.choice(scalars)
+    r = rng.random()
+    a = _rand_expr(rng, depth - 1, rank, scalars)
+    b = _rand_expr(rng, depth - 1, rank, scalars)
+    if r < 0.12:
+        return f"abs({a})"
+    if r < 0.20:
+        return f"sqrt(abs({a}))"
+    if r < 0.27:
+        return f"min({a}, {b})"
+    if r < 0.34:
+        return f"max({a}, {b}, {_rand_expr(rng, 0, rank, scalars)})"
+    op = rng.choice(["+", "-", "*", "/"])
+    return f"({a} {op} {b})"
+
+
+def gen_random():
+    rng = random.Random(20260823)
+    nrng = np.random.default_rng(12)
+    arrays = {}
+    meta = []
+    for trial in range(60):
+        rank = 2 if trial < 40 else (3 if trial < 52 else 1)
+        use_scalars = trial % 3 == 0
+        scal_names = ["c", "q"] if use_scalars else []
+        body = ""
+        decls = ""
+        if use_scalars:
+            decls += "  real :: c\n  integer :: q\n"
+        if trial % 4 == 1:
+            decls += "  real :: t\n"
+            body += "  t = " + _rand_expr(rng, 2, rank, scal_names) + "\n"
+            scal_names = scal_names + ["t"]
+        body += ("  U(" + ",".join(["0"] * rank) + ") = "
+                 + _rand_expr(rng, 3, rank, scal_names) + "\n")
+        if trial % 5 == 2:
+            body += ("  U(" + ",".join(["0"] * rank) + ") = U(" + ",".join(["0"] * rank)
+                     + ") * 0.5 + " + f"{rng.uniform(0.25, 2.0):.3f}" + "\n")
+        dims = ",".join([":"] * rank)
+        halo = ", ".join(["2:*:2"] * rank)
+        params = "U" + (", c, q" if use_scalars else "")
+        text = (f"pure concurrent subroutine k({params})\n"
+                f"  real, dimension({dims}), HALO({halo}) :: U\n{decls}{body}"
+                f"end subroutine k\n\nprogram main\nend program main\n")
+        result = compile_text(text)
+        kir = lower_kernel(result.kernels["k"])
+        shape = {1: (11,), 2: (9, 7), 3: (7, 6, 5)}[rank]
+        field = nrng.uniform(-1, 1, shape)
+        scal = {"c": np.float64(0.75), "q": np.int64(3)} if use_scalars else {}
+        with np.errstate(all="ignore"):
+            out = oracle_step(field, kir, scal)
+        arrays[f"r{trial}_in"] = field
+        arrays[f"r{trial}_out"] = out
+        meta.append({"trial": trial, "rank": rank, "source": text,
+                     "ir": serialize(from_lopec(kir)),
+                     "scalars": {"c": 0.75, "q": 3} if use_scalars else {}})
+    np.savez_compressed(HERE / "random.npz", **arrays)
+    (HERE / "random.json").write_text(json.dumps(meta, indent=1) + "\n")
+
+
+def gen_kats():
+    lap = compile_text((CORPUS / "laplacian.lope").read_text(), "laplacian.lope")
+    kats = {}
+    f = np.zeros((4, 4)); f[1, 1] = 1.0
+    kats["point_source"] = run_machine(lap, f, images=1, steps=1).gather().tolist()
+    f = np.zeros((4, 4)); f[0, 0] = 1.0
+    kats["corner_source"] = run_machine(lap, f, images=1, steps=1).gather().tolist()
+    f = np.full((8, 8), 1.0)
+    kats["fixed_point_ones_25"] = bool(np.array_equal(
+        run_machine(lap, f.copy(), images=1, steps=25).gather(), f))
+    lay = StorageLayout((8, 4), (1, 1), (1, 1))
+    kats["layout_12"] = map_local_to_global((1, 0), (1, 1), lay)
+    kats["layout_59"] = map_local_to_global((1, 1), (8, 4), lay)
+    # sub-range launch: only i=2:M-1, j=3:N updated, the rest copied through
+    sub = compile_text("""\
+pure concurrent subroutine k(U)
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: U
+  U(0,0) = U(0,0)*0.5 + U(-1,0) - U(0,+1)*0.25
+end subroutine k
+
+program main
+  real, allocatable, dimension(:,:), codimension[:,:], HALO(1:*:1,1:*:1) :: U
+  integer :: device
+  integer :: it
+  device = GET_SUBIMAGE(1)
+  allocate(U(0:M+1, 0:N+1)[MP,*])
+  do it = 1, nsteps
+    call HALO_TRANSFER(U, BC=CYCLIC)
+    do concurrent (i=2:M-1, j=3:N) [[device]]
+      call k( U(i,j)[device] )
+    end do
+  end do
+end program main
+""")
+    rng = np.random.default_rng(55)
+    f = rng.uniform(-1, 1, (10, 9))
+    m = run_machine(sub, f.copy(), images=1, steps=3)
+    kats["subrange_in"] = f.tolist()
+    kats["subrange_out_padded"] = m.arrays["u"].view(1).tolist()
+    kats["subrange_ir"] = serialize(from_lopec(lower_kernel(sub.kernels["k"])))
+    twice = compile_text("""\
+pure concurrent subroutine twice(U)
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: U
+  U(0,0) = U(0,0)*2
+  U(0,0) = U(0,0) + 1
+end subroutine twice
+
+program main
+end program main
+""")
+    kats["twice_ir"] = serialize(from_lopec(lower_kernel(twice.kernels["twice"])))
+    # two-array kernel: reads V at offsets, stores U and V (pending centre of U)
+    two = compile_text("""\
+pure concurrent subroutine mix(U, V)
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: U
+  real, dimension(:,:), HALO(1:*:1, 1:*:1) :: V
+  U(0,0) = U(0,0) + 0.5*V(-1,0) - V(0,+1)
+  V(0,0) = V(0,0)*0.25 + U(0,0)
+end subroutine mix
+
+program main
+  real, allocatable, dimension(:,:), codimension[:,:], HALO(1:*:1,1:*:1) :: U
+  real, allocatable, dimension(:,:), codimension[:,:], HALO(1:*:1,1:*:1) :: V
+  integer :: device
+  integer :: it
+  device = GET_SUBIMAGE(1)
+  allocate(U(0:M+1, 0:N+1)[MP,*])
+  allocate(V(0:M+1, 0:N+1)[MP,*])
+  V(:,:) = U(:,:)
+  do it = 1, nsteps
+    call HALO_TRANSFER(U, BC=CYCLIC)
+    call HALO_TRANSFER(V, BC=CYCLIC)
+    do concurrent (i=1:M, j=1:N) [[device]]
+      call mix( U(i,j)[device], V(i,j)[device] )
+    end do
+  end do
+end program main
+""")
+    f = rng.uniform(-1, 1, (8, 6))
+    m = run_machine(two, f.copy(), images=1, steps=4)
+    kats["mix_in"] = f.tolist()
+    kats["mix_out_u"] = m.arrays["u"].view(1).tolist()
+    kats["mix_out_v"] = m.arrays["v"].view(1).tolist()
+    kats["mix_ir"] = serialize(from_lopec(lower_kernel(two.kernels["mix"])))
+    (HERE / "kats.json").write_text(json.dumps(kats, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    gen_kernels()
+    gen_runs()
+    gen_exchange()
+    gen_random()
+    gen_kats()
+    for p in sorted(HERE.iterdir()):
+        print(p.name, p.stat().st_size)
