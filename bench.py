@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the LOPe stencil hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl ours|reference]
+
+A *step* is one iteration of ``do it: HALO_TRANSFER(U); do concurrent ... call
+K(U)`` over the whole field: one fused liblope_b200.so kernel (launch of step t
+plus the periodic halo refresh for step t+1), and at N > 1 the NVLink face
+exchange of the partitioned dimension.
+
+Workloads (BASELINE.json configs; default c3, the HBM-roofline headline):
+  c1  heat2d   1024^2      fp32  (L2-resident, launch-bound)
+  c2  ninept2d 16384^2     fp32
+  c3  lap3d7   1024^3      fp32  per GPU (N>1: slab-decomposed along z, weak scaling)
+  c4  box5x5   32768^2     fp64  (N>1: 32768 x 32768*N, slabs along y, weak scaling)
+  c5  lap3d7   2048^3      fp32  per GPU
+
+``value`` = interior points x steps (all ranks) / max-over-ranks device time,
+in Gpoints/s.  ``e2e`` = the same metric through the public API with the field
+in pinned host memory: H2D upload, ``E2E_ITERS`` iterations, D2H download, all
+inside the timed region.  ``roofline`` compares the dominant kernel's
+algorithmic bytes (2 x sizeof(T) per point update) per launch / its
+CUDA-event duration with the measured HBM copy bandwidth.
+
+``--impl reference`` times the reference algorithm on the host CPU (the numpy
+port of lopec's vectorised launch in oracle/, all host threads) on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import sys
+import threading
+import time
+
+REPO = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+WORKLOADS = {
+    "c1": dict(kernel="heat2d", shape=(1024, 1024), dtype="float32", split=1,
+               desc="2D 5-point heat 1024x1024 fp32, halo 1 (config 1)"),
+    "c2": dict(kernel="ninept2d", shape=(16384, 16384), dtype="float32", split=1,
+               desc="2D 9-point 16384x16384 fp32, halo 1 (config 2)"),
+    "c3": dict(kernel="lap3d7", shape=(1024, 1024, 1024), dtype="float32", split=2,
+               desc="3D 7-point 1024^3 fp32 per GPU, halo 1 (config 3; N>1 weak-scaled slabs along z)"),
+    "c4": dict(kernel="box5x5", shape=(32768, 32768), dtype="float64", split=1,
+               desc="2D 5x5 box 32768x32768 fp64 per GPU, halo 2 (config 4; N>1 slabs along y)"),
+    "c5": dict(kernel="lap3d7", shape=(2048, 2048, 2048), dtype="float32", split=2,
+               desc="3D 7-point 2048^3 fp32 per GPU, halo 1 (config 5, weak scaling)"),
+}
+E2E_ITERS = 100
+SEED = 20260823
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            if workload in d:
+                return d[workload]
+        except Exception:
+            pass
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:    # pragma: no cover - depends on the box
+            log("clock sampling unavailable:", e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+        return False
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the numpy port of the reference's vectorised launch)
+
+
+def cpu_reference(wl, seconds=10.0, max_steps=None):
+    """Time the reference algorithm (halo transfer + run_body launch, fp as the workload)
+    on a bounded sample: the first planes of the workload's field along the
+    slowest axis, all host threads."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import lope_oracle as O
+    from paper_1502_03504_b200 import stencils
+
+    kir = stencils.by_name(wl["kernel"])
+    npdt = np.float32 if wl["dtype"] == "float32" else np.float64
+    shape = list(wl["shape"])
+    # bounded sample: keep the leading dims, cut the slowest one to ~32M points
+    inner = int(np.prod(shape[:-1]))
+    shape[-1] = max(4, min(shape[-1], (1 << 25) // inner))
+    if len(shape) == 2 and inner > (1 << 24):
+        shape = [1 << 14, 1 << 11]
+    fp = kir.footprints[kir.array_params[0]].dims
+    lo, hi = [n for n, _ in fp], [p for _, p in fp]
+    f = O.hash_field(tuple(shape[::-1]), SEED, npdt).T     # C-ordered block, reference index order
+    blk = O.embed(np.ascontiguousarray(f), lo, hi, npdt)
+    threads = os.cpu_count() or 1
+    pool = ThreadPoolExecutor(threads)
+    O.threaded_machine_step(blk, lo, hi, kir, None, npdt, pool, threads)     # warm-up
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        O.threaded_machine_step(blk, lo, hi, kir, None, npdt, pool, threads)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (max_steps and n >= max_steps):
+            break
+    pts = int(np.prod(shape))
+    return {"value": pts * n / el / 1e9, "unit": "Gpoints/s", "cores": threads, "kind": "port",
+            "sample": f"{n} step(s) of {kir.name} on {'x'.join(map(str, shape))} {wl['dtype']} "
+                      f"(numpy port of lopec Machine._halo_exchange + _launch_vector, "
+                      f"{threads} threads), {el:.1f} s"}
+
+
+def run_reference_arm(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    steps, warm = args.steps, args.warmup
+    # each step: a bounded CPU sample; scale to a few minutes in total
+    per = max(0.5, min(5.0, 120.0 / max(1, steps + warm)))
+    cpu_reference(wl, seconds=per * warm if warm else 0.1, max_steps=max(1, warm))
+    res = cpu_reference(wl, seconds=per * steps, max_steps=steps)
+    line = {
+        "metric": "stencil Gpoints/s & HBM GB/s (% of 8 TB/s roofline) at 1/2/4/8 B200 vs CPU ref",
+        "impl": "reference", "value": res["value"], "unit": "Gpoints/s", "n_gpus": ws,
+        "steps": steps, "warmup": warm, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "float32" else "f64",
+        "data": "synthetic (splitmix64 U(-1,1) field)",
+        "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
+                   "shape_per_gpu": list(wl["shape"])},
+        "cpu_baseline": res,
+        "e2e": {"value": res["value"], "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def run_gpu_arm(args, wl):
+    import numpy as np
+    import torch
+
+    from paper_1502_03504_b200 import _lib, stencils
+    from paper_1502_03504_b200 import runtime as R
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    kir = stencils.by_name(wl["kernel"])
+    kern = R.CompiledKernel(kir, wl["dtype"])
+    fp = kir.footprints[kir.array_params[0]].dims
+    lo, hi = [n for n, _ in fp], [p for _, p in fp]
+    shape = tuple(wl["shape"])
+    esz = 4 if wl["dtype"] == "float32" else 8
+    points = int(np.prod(shape))
+    stream = torch.cuda.current_stream()
+
+    if ws > 1:
+        from paper_1502_03504_b200 import dist as D
+        field = D.SlabArray(shape, lo, hi, wl["dtype"], group=group)
+        gext = list(shape[:-1]) + [shape[-1] * ws]
+        gorg = [0] * (len(shape) - 1) + [shape[-1] * rank]
+        field.block.fill_hash(SEED, gext, gorg)
+        stepper = D.SlabStepper(kern, field)
+        stepper.exchange()
+
+        def do_step():
+            stepper.step()
+        arr = field.block
+    else:
+        arr = R.HaloArray(shape, lo, hi, wl["dtype"])
+        arr.fill_hash(SEED)
+        R.halo_transfer(arr)
+
+        def do_step():
+            R.step(kern, arr)
+
+    for _ in range(args.warmup):
+        do_step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # timed region: exactly K steps, per-step events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t_all0, t_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    barrier()
+    with ClockSampler(local) as clk:
+        t_all0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            do_step()
+            ev[i][1].record(stream)
+        t_all1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - l0
+    total_ms = t_all0.elapsed_time(t_all1)
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = points * ws * args.steps / (total_ms / 1e3) / 1e9
+
+    # dominant kernel: the fused step kernel, one launch per step at N=1
+    kernel_ms = sorted(per_step)[len(per_step) // 2] if ws == 1 else None
+    if ws > 1:
+        kernel_ms = stepper.kernel_ms_estimate()
+    alg_bytes = 2 * esz * points
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
+                "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
+                "kernel_ms": round(kernel_ms, 4),
+                "pct_of_8TBs": round(100 * alg_bytes / (kernel_ms / 1e3) / 8e12, 1)}
+
+    # e2e through the public API, host buffers, H2D + E2E_ITERS iterations + D2H timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_reference(wl, seconds=args.cpu_seconds)
+
+    del arr
+    if rank == 0:
+        line = {
+            "metric": "stencil Gpoints/s & HBM GB/s (% of 8 TB/s roofline) at 1/2/4/8 B200 vs CPU ref",
+            "value": round(value, 3), "unit": "Gpoints/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if wl["dtype"] == "float32" else "f64",
+            "data": "synthetic (splitmix64 U(-1,1) field generated on device)",
+            "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
+                       "shape_per_gpu": list(shape), "global_shape": list(shape[:-1]) + [shape[-1] * ws],
+                       "halo": [lo, hi], "parallelism": f"slab{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
+                             else "L2-resident working set (config 1); HBM fraction informational",
+                       "hbm_gbs_alg": round(alg_bytes * ws / (ms_per_step / 1e3) / 1e9 / ws, 1)},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev):
+    """Public API, host (pinned) buffers: upload, E2E_ITERS iterations, download."""
+    import numpy as np
+    import torch
+
+    from paper_1502_03504_b200 import runtime as R
+
+    nbytes = int(np.prod(shape)) * esz
+    tdt = torch.float32 if esz == 4 else torch.float64
+    host_in = torch.empty(nbytes // esz, dtype=tdt, pin_memory=True)
+    host_in.numpy()[:] = 0.5
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    if ws > 1:
+        from paper_1502_03504_b200 import dist as D
+
+        def call():
+            D.run_pinned(kern, shape, lo, hi, wl["dtype"], host_in, host_out, E2E_ITERS, group)
+    else:
+        def call():
+            R.run_pinned(kern, shape, lo, hi, wl["dtype"], host_in, host_out, E2E_ITERS)
+    call()                              # warm-up (allocation, module load)
+    torch.cuda.synchronize()
+    reps = 2
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        call()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    pts = int(np.prod(shape)) * ws * E2E_ITERS * reps
+    return {"value": round(pts / el / 1e9, 3), "unit": "Gpoints/s",
+            "h2d_bytes_per_step": nbytes // E2E_ITERS, "d2h_bytes_per_step": nbytes // E2E_ITERS,
+            "iters_per_call": E2E_ITERS, "calls": reps, "seconds": round(el, 4),
+            "api": "runtime.run_pinned (HaloArray upload, iterate, gather)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: fewer than 3 warm-up steps")
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_gpu_arm(args, wl)
+
+
+if __name__ == "__main__":
+    main()

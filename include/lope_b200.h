@@ -1,0 +1,127 @@
+/* lope_b200.h — C ABI of the B200-native LOPe stencil hot path (liblope_b200.so).
+ *
+ * The reference (/root/reference/pkg, package `lopec`) is pure Python and has no
+ * FFI.  Its hot path sits behind three methods of `Machine`; each
+ * entry point below replaces one of them, and INTEGRATION.md shows the ctypes
+ * binding a lopec maintainer would add:
+ *
+ *   lope_kernel_compile   replaces ir.lower_kernel -> run_body's tree walk
+ *                         (lopec/ir.py:140-182, 258-308): the LOPE1 text of a
+ *                         KernelIR is compiled once (NVRTC, sm_100a, cached).
+ *   lope_launch           replaces Machine._launch_vector (runtime.py:596-618):
+ *                         snapshot reads, centre stores over a launch range,
+ *                         everything outside the range copied through.
+ *   lope_halo_fill        replaces Machine._halo_exchange (runtime.py:643-697)
+ *                         for dimensions whose neighbour is the image itself.
+ *   lope_step             a launch over the full interior fused with the next
+ *                         HALO_TRANSFER's local (periodic) fill.
+ *   lope_layout_init / lope_pack / lope_unpack
+ *                         replace StorageLayout + _scatter_block / gather
+ *                         (ir.py:189-230, runtime.py:477-486, 715-737).
+ *
+ * Conventions: every call returns 0 on success, otherwise a positive reference
+ * E-code number (102 footprint exceeds halo, 108 shape/range, 201 grid, 202
+ * unallocated) or a negative CUDA / NVRTC / driver error; the message is in
+ * lope_last_error().  Buffers are owned by the caller (device pointers from
+ * cudaMalloc / torch); `stream` is a cudaStream_t.  Calls are asynchronous on
+ * the given stream.
+ */
+#ifndef LOPE_B200_H
+#define LOPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOPE_ABI_VERSION 1
+
+#define LOPE_F32 1
+#define LOPE_F64 2
+
+/* Device storage of one image's block: the reference's padded column-major block
+ * (ir.py:189-230: padded_d = m_d + lo_d + hi_d, dim 1 fastest) with the row pitch
+ * rounded up to 16 bytes (TMA stride rule).  Element at 0-based padded
+ * coordinates (c0,c1,c2) is at c0 + c1*stride[1] + c2*stride[2]. */
+typedef struct lope_layout {
+  int32_t rank;          /* 1..3 */
+  int32_t dtype;         /* LOPE_F32 | LOPE_F64 */
+  int64_t interior[3];   /* m_d; 1 for d >= rank */
+  int32_t lo[3];         /* halo widths (0..8); 0 for d >= rank */
+  int32_t hi[3];
+  int64_t padded[3];     /* m_d + lo_d + hi_d */
+  int64_t stride[3];     /* element strides: 1, row pitch, plane pitch */
+  int64_t count;         /* elements to allocate */
+  int64_t elem_bytes;
+} lope_layout;
+
+typedef struct lope_kernel lope_kernel;
+
+int lope_abi_version(void);
+const char* lope_last_error(void);
+
+/* Cache directory for compiled cubins (default: $LOPE_CACHE_DIR or none). */
+int lope_set_cache_dir(const char* path);
+
+/* StorageLayout(interior, lo, hi) of ir.py:189 -> device layout.  E108 on bad
+ * shapes (interior < 1, widths outside 0..8). */
+int lope_layout_init(lope_layout* out, int32_t rank, int32_t dtype, const int64_t* interior,
+                     const int32_t* lo, const int32_t* hi);
+
+/* Compile a kernel from its LOPE1 text (paper_1502_03504_b200/ir.py: serialize). */
+int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kernel** out);
+int lope_kernel_destroy(lope_kernel* k);
+/* JSON description: arrays, scalars, stored arrays, footprints, path chosen. */
+int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n);
+/* Emitted CUDA source of the kernel (for inspection / tests). */
+int lope_kernel_source(const lope_kernel* k, char* buf, size_t n);
+
+/* Machine._launch_vector: one launch over ranges[d] = {lo_d, hi_d} (1-based,
+ * inclusive; rank entries).  in[a]: the snapshot of array parameter a; out[a]:
+ * its live buffer (must differ from in[a]) or NULL when the kernel never stores
+ * it.  After the call out[a] equals in[a] except over the range, where it holds
+ * the kernel's centre values.  rscal / iscal hold the scalar parameters in
+ * declaration order (real ones read from rscal, integer ones from iscal). */
+int lope_launch(const lope_kernel* k, const lope_layout* layouts, const int64_t* ranges,
+                const void* const* in, void* const* out, const double* rscal, const int64_t* iscal,
+                void* stream);
+
+/* Fused full-interior launch + periodic halo refresh of the dims in wrap_mask
+ * (bit d = dim d+1).  Precondition: in's halos are valid.  Postcondition: out's
+ * interior is the new field and its halo cells along wrap_mask dims hold the
+ * periodic images of it — the state after the next HALO_TRANSFER.  One array
+ * parameter only. */
+int lope_step(const lope_kernel* k, const lope_layout* layout, const void* in, void* out,
+              const double* rscal, const int64_t* iscal, int32_t wrap_mask, void* stream);
+
+/* _halo_exchange with every neighbour equal to self along the dims in dims_mask:
+ * each halo cell gets its periodic image (in place).  E108 if a halo is wider
+ * than the interior. */
+int lope_halo_fill(const lope_layout* layout, void* buf, int32_t dims_mask, void* stream);
+
+/* Copy the interior between a host column-major array (m0 x m1 x m2, dim 1
+ * fastest — numpy order='F') and the device block. */
+int lope_pack(const lope_layout* layout, const void* host, void* dev, void* stream);
+int lope_unpack(const lope_layout* layout, const void* dev, void* host, void* stream);
+
+/* Fill the interior with the synthetic U(-1,1) field: value of global cell
+ * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
+ * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */
+int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const int64_t* global_extent,
+                   const int64_t* global_origin, void* stream);
+
+/* Offset/count (elements) of a contiguous face slab along the slowest dim
+ * (d = rank-1): which = 0 low halo, 1 high halo, 2 first `hi` interior planes,
+ * 3 last `lo` interior planes.  Used to exchange faces between slab partitions. */
+int lope_face_span(const lope_layout* layout, int32_t which, int64_t* offset, int64_t* count);
+
+/* Number of this library's kernels launched since load (evidence for the bench). */
+int64_t lope_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOPE_B200_H */

@@ -330,3 +330,48 @@ def first_mismatch(a, b):
 
 def gpts(points, seconds):
     return points / seconds / 1e9 if seconds > 0 else math.inf
+
+
+# ---------------------------------------------------------------------------
+# The CPU baseline leg of bench.py: the reference's vectorised launch
+# (runtime.py:596-618 via run_body) over one image, split along the slowest axis
+# across host threads (numpy releases the GIL inside ufunc loops).
+
+
+def threaded_machine_step(blk, lo, hi, kir, scalars=None, dtype=np.float64, pool=None, nthreads=1):
+    """One ``HALO_TRANSFER`` + full-interior launch on padded block ``blk`` (in place).
+
+    The launch range is split along the block's slowest-varying memory axis
+    (axis 0 for the C-ordered blocks used here) so each thread streams its own
+    contiguous chunk; the arithmetic is ``run_body``'s, unchanged.
+    """
+    halo_fill(blk, lo, hi)
+    snap = blk.copy()                                   # runtime.py:596 snapshot
+    shape = tuple(s - a - b for s, a, b in zip(blk.shape, lo, hi))
+    ax = 0 if blk.flags.c_contiguous else blk.ndim - 1
+    n = shape[ax]
+    plane = max(1, int(np.prod(shape)) // n)
+    chunk = max(1, (1 << 17) // plane)              # ~128K points per chunk: temporaries stay in cache
+    bounds = [(z, min(n, z + chunk)) for z in range(0, n, chunk)]
+    name = kir.array_params[0]
+
+    def work(b):
+        z0, z1 = b
+        if z0 >= z1:
+            return
+        ranges = [(1, m) for m in shape]
+        ranges[ax] = (z0 + 1, z1)
+
+        def read(_name, offsets):
+            return snap[tuple(slice(a - 1 + h + o, e + h + o)
+                              for (a, e), h, o in zip(ranges, lo, offsets))]
+
+        pending = run_body(kir, read, scalars, dtype)
+        blk[tuple(slice(a - 1 + h, e + h) for (a, e), h in zip(ranges, lo))] = pending[name]
+
+    if pool is None or nthreads <= 1:
+        for b in bounds:
+            work(b)
+    else:
+        list(pool.map(work, bounds))
+    return blk

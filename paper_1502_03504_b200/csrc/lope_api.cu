@@ -1,0 +1,885 @@
+// lope_api.cu — liblope_b200.so: the C ABI of include/lope_b200.h.
+//
+// Host side: layout arithmetic, argument checks with the reference's error codes,
+// NVRTC compilation of IR-specialised kernels for sm_100a (cached on disk and per
+// device), TMA descriptor encoding, and launches through the driver API (entry
+// points fetched with cudaGetDriverEntryPoint, so the library loads on machines
+// without a GPU driver).  Device side (compiled here by nvcc for sm_100a): the
+// periodic halo fill, the copy-through of cells outside a launch range, and the
+// synthetic-input generator.  The body-specialised stencil kernels live in
+// lope_device.cuh and are compiled at run time.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <vector>
+
+#include "../../include/lope_b200.h"
+#include "lope_codegen.h"
+
+static const char* kDeviceSrc =
+#include "lope_device_src.inc"
+    ;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+std::mutex g_mu;
+std::string g_cache_dir;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(-(int)e_, "%s failed: %s", #expr, cudaGetErrorString(e_));             \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Driver API entry points
+
+struct Drv {
+  bool ok = false;
+  std::string why;
+  decltype(&cuModuleLoadData) moduleLoadData = nullptr;
+  decltype(&cuModuleGetFunction) moduleGetFunction = nullptr;
+  decltype(&cuModuleGetGlobal) moduleGetGlobal = nullptr;
+  decltype(&cuModuleUnload) moduleUnload = nullptr;
+  decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
+  decltype(&cuLaunchKernel) launchKernel = nullptr;
+  decltype(&cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
+  decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
+  decltype(&cuGetErrorString) getErrorString = nullptr;
+};
+
+Drv& drv() {
+  static Drv d;
+  static bool inited = false;
+  if (inited) return d;
+  inited = true;
+  auto get = [&](const char* name, void** fn) -> bool {
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn) {
+      d.why = std::string("driver entry point ") + name + " unavailable";
+      return false;
+    }
+    return true;
+  };
+  d.ok = get("cuModuleLoadData", (void**)&d.moduleLoadData) &&
+         get("cuModuleGetFunction", (void**)&d.moduleGetFunction) &&
+         get("cuModuleGetGlobal", (void**)&d.moduleGetGlobal) &&
+         get("cuModuleUnload", (void**)&d.moduleUnload) &&
+         get("cuFuncSetAttribute", (void**)&d.funcSetAttribute) &&
+         get("cuLaunchKernel", (void**)&d.launchKernel) &&
+         get("cuTensorMapEncodeTiled", (void**)&d.tensorMapEncodeTiled) &&
+         get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occupancy) &&
+         get("cuGetErrorString", (void**)&d.getErrorString);
+  return d;
+}
+
+int cu_fail(CUresult r, const char* what) {
+  const char* s = nullptr;
+  if (drv().getErrorString) drv().getErrorString(r, &s);
+  return fail(-1000 - (int)r, "%s failed: %s", what, s ? s : "unknown driver error");
+}
+
+// ---------------------------------------------------------------------------
+// Device-side layout mirror used by the AOT kernels
+
+struct DevLayout {
+  int rank;
+  int m[3], lo[3], hi[3];
+  long long P[3];
+  long long S1, S2;
+};
+
+DevLayout dev_layout(const lope_layout* L) {
+  DevLayout d;
+  d.rank = L->rank;
+  for (int i = 0; i < 3; ++i) {
+    d.m[i] = (int)L->interior[i];
+    d.lo[i] = L->lo[i];
+    d.hi[i] = L->hi[i];
+    d.P[i] = L->padded[i];
+  }
+  d.S1 = L->stride[1];
+  d.S2 = L->stride[2];
+  return d;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// AOT kernels (nvcc, sm_100a)
+
+__device__ __forceinline__ int lope_wrapc(int c, int lo, int m) {
+  int i = c - lo;
+  if (i < 0) i += m;
+  else if (i >= m) i -= m;
+  return i + lo;
+}
+
+// Periodic halo fill in place: every halo cell (along the masked dims) receives
+// its periodic image.  One warp per padded row (c1, c2).
+template <class T>
+__global__ void __launch_bounds__(256) lope_k_halo_fill(T* __restrict__ buf, DevLayout L, int mask) {
+  const long long nrows = L.P[1] * L.P[2];
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < nrows; r += nw) {
+    const int c1 = (int)(r % L.P[1]);
+    const int c2 = (int)(r / L.P[1]);
+    const int s1 = (mask & 2) ? lope_wrapc(c1, L.lo[1], L.m[1]) : c1;
+    const int s2 = (mask & 4) ? lope_wrapc(c2, L.lo[2], L.m[2]) : c2;
+    T* dst = buf + c1 * L.S1 + c2 * L.S2;
+    const T* src = buf + s1 * L.S1 + s2 * L.S2;
+    if (s1 != c1 || s2 != c2) {
+      for (int x = lane; x < L.P[0]; x += 32)
+        dst[x] = src[(mask & 1) ? lope_wrapc(x, L.lo[0], L.m[0]) : x];
+    } else if (mask & 1) {
+      const int nh = L.lo[0] + L.hi[0];
+      for (int q = lane; q < nh; q += 32) {
+        const int x = q < L.lo[0] ? q : L.m[0] + L.lo[0] + (q - L.lo[0]);
+        dst[x] = src[lope_wrapc(x, L.lo[0], L.m[0])];
+      }
+    }
+  }
+}
+
+// out := in for every padded cell outside the half-open box [b, e) (padded coords).
+template <class T>
+__global__ void __launch_bounds__(256) lope_k_copy_through(const T* __restrict__ in, T* __restrict__ out,
+                                                           DevLayout L, int b0, int e0, int b1, int e1,
+                                                           int b2, int e2) {
+  const long long nrows = L.P[1] * L.P[2];
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < nrows; r += nw) {
+    const int c1 = (int)(r % L.P[1]);
+    const int c2 = (int)(r / L.P[1]);
+    const long long base = c1 * L.S1 + c2 * L.S2;
+    const bool inrow = c1 >= b1 && c1 < e1 && c2 >= b2 && c2 < e2;
+    if (!inrow) {
+      for (int x = lane; x < L.P[0]; x += 32) out[base + x] = in[base + x];
+    } else {
+      for (int x = lane; x < b0; x += 32) out[base + x] = in[base + x];
+      for (int x = e0 + lane; x < L.P[0]; x += 32) out[base + x] = in[base + x];
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long lope_splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) lope_k_fill_hash(T* __restrict__ buf, DevLayout L, unsigned long long seed,
+                                                        long long G0, long long G1, long long o0, long long o1,
+                                                        long long o2) {
+  const long long n = (long long)L.m[0] * L.m[1] * L.m[2];
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % L.m[0];
+    const long long rr = t / L.m[0];
+    const long long j = rr % L.m[1];
+    const long long k = rr / L.m[1];
+    const unsigned long long g = (unsigned long long)((o0 + i) + G0 * ((o1 + j) + G1 * (o2 + k)));
+    const unsigned long long z = lope_splitmix64(g + seed * 0x9E3779B97F4A7C15ULL);
+    const double v = (double)(z >> 11) * (1.0 / 9007199254740992.0);
+    const double u = 2.0 * v - 1.0;
+    buf[(i + L.lo[0]) + (j + L.lo[1]) * L.S1 + (k + L.lo[2]) * L.S2] = (T)u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compiled kernels
+
+namespace {
+
+struct TileCfg {
+  int bxw = 4, wy = 2, ry = 8, ns = 8;
+};
+
+struct DevMod {
+  CUmodule mod = nullptr;
+  CUfunction generic = nullptr;
+  CUfunction tiled = nullptr;
+  int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
+};
+
+// host mirrors of the device parameter structs (lope_device.cuh)
+template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
+template <class T> struct HScal { T v[16]; };
+struct HGeom {
+  int ext[3], m[3], r0[3], lo[3], hi[3];
+  int wrap, zchunk;
+};
+
+}  // namespace
+
+struct lope_kernel {
+  lope::Kir ir;
+  int dtype = LOPE_F32;
+  bool tiled_ok = false;
+  TileCfg tile;
+  std::string source;
+  std::vector<char> cubin;
+  std::map<int, DevMod> mods;
+  std::string describe_path;
+};
+
+namespace {
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ULL) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+bool read_file(const std::string& p, std::vector<char>* out) {
+  std::ifstream f(p, std::ios::binary);
+  if (!f) return false;
+  out->assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  return !out->empty();
+}
+
+void write_file_atomic(const std::string& p, const std::vector<char>& data) {
+  std::string tmp = p + ".tmp." + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    f.write(data.data(), (std::streamsize)data.size());
+  }
+  std::rename(tmp.c_str(), p.c_str());
+}
+
+TileCfg pick_tile(const lope::Kir& k, int dtype) {
+  TileCfg c;
+  if (dtype == LOPE_F32) {
+    if (k.rank == 3) { c.bxw = 4; c.wy = 2; c.ry = 8; }
+    else             { c.bxw = 4; c.wy = 4; c.ry = 8; }
+  } else {
+    if (k.rank == 3) { c.bxw = 2; c.wy = 2; c.ry = 8; }
+    else             { c.bxw = 2; c.wy = 4; c.ry = 8; }
+  }
+  int nzw = k.fn[0][2] + k.fp[0][2] + 1;
+  c.ns = k.rank == 3 ? nzw + 5 : 4;
+  if (const char* e = std::getenv("LOPE_TILE")) {
+    int a, b, cc, d;
+    if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &cc, &d) == 4) {
+      c.bxw = a; c.wy = b; c.ry = cc; c.ns = d < nzw + 1 ? nzw + 1 : d;
+    }
+  }
+  return c;
+}
+
+int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
+  int sz = dtype == LOPE_F32 ? 4 : 8;
+  int vec = 16 / sz;
+  int bx = 32 * c.bxw, by = c.wy * c.ry;
+  int boxx = ((k.fn[0][0] + bx + k.fp[0][0] + vec - 1) / vec) * vec;
+  int boxy = by + k.fn[0][1] + k.fp[0][1];
+  int stage = ((boxx * boxy * sz + 127) / 128) * 128;
+  if (boxx > 256 || boxy > 256) return 1 << 30;
+  return c.ns * stage + c.ns * 8;
+}
+
+std::string build_source(lope_kernel* K) {
+  const lope::Kir& k = K->ir;
+  std::ostringstream s;
+  s << kDeviceSrc << "\n";
+  s << lope::emit_body(k) << "\n";
+  const char* T = K->dtype == LOPE_F32 ? "float" : "double";
+  s << "typedef " << T << " LT;\n";
+  s << "struct LopeArrPack { LopeArr<LT> a[" << k.arrays.size() << "]; };\n";
+  s << "extern \"C\" __global__ void __launch_bounds__(256) lope_generic("
+       "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
+       "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n}\n";
+  if (K->tiled_ok) {
+    const TileCfg& c = K->tile;
+    s << "typedef LopeTiledCfg<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
+      << "> LopeCfg;\n";
+    s << "extern \"C\" __constant__ int lope_tiled_info[4] = {LopeCfg::SMEM_BYTES, LopeCfg::THREADS, "
+         "LopeCfg::BOXX, LopeCfg::BOXY};\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * c.bxw * c.wy
+      << ", 2) lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
+         "const LopeScal<LT> sc, const LopeGeom g) {\n"
+      << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
+      << ">(&map, a, sc, g);\n}\n";
+  }
+  return s.str();
+}
+
+int nvrtc_compile(const std::string& src, const std::string& name, std::vector<char>* cubin) {
+  std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-fmad=false",
+                                   "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-lineinfo",
+                                   "-DNDEBUG"};
+  int ver_major = 0, ver_minor = 0;
+  nvrtcVersion(&ver_major, &ver_minor);
+  std::string key = src;
+  for (auto& o : opts) key += "\n" + o;
+  key += "\nnvrtc " + std::to_string(ver_major) + "." + std::to_string(ver_minor);
+  char hbuf[32];
+  std::snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)fnv1a(key));
+  std::string dir;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    dir = g_cache_dir;
+  }
+  if (dir.empty()) {
+    if (const char* e = std::getenv("LOPE_CACHE_DIR")) dir = e;
+  }
+  std::string path;
+  if (!dir.empty()) {
+    path = dir + "/" + name + "-" + hbuf + ".cubin";
+    if (read_file(path, cubin)) return 0;
+  }
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(-2000 - (int)r, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  std::vector<const char*> copts;
+  for (auto& o : opts) copts.push_back(o.c_str());
+  r = nvrtcCompileProgram(prog, (int)copts.size(), copts.data());
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    if (log.size() > 1800) log = log.substr(0, 1800);
+    return fail(-2000 - (int)r, "NVRTC compile of kernel '%s' failed: %s", name.c_str(), log.c_str());
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  if (!path.empty()) {
+    mkdir(dir.c_str(), 0755);
+    write_file_atomic(path, *cubin);
+  }
+  return 0;
+}
+
+int get_mod(lope_kernel* K, DevMod** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  auto it = K->mods.find(dev);
+  if (it != K->mods.end()) {
+    *out = &it->second;
+    return 0;
+  }
+  Drv& d = drv();
+  if (!d.ok) return fail(-3, "CUDA driver API unavailable: %s", d.why.c_str());
+  CUDA_TRY(cudaFree(nullptr));   // make the primary context current on this thread
+  DevMod m;
+  CUresult r = d.moduleLoadData(&m.mod, K->cubin.data());
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleLoadData");
+  r = d.moduleGetFunction(&m.generic, m.mod, "lope_generic");
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_generic)");
+  if (K->tiled_ok) {
+    r = d.moduleGetFunction(&m.tiled, m.mod, "lope_tiled");
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_tiled)");
+    CUdeviceptr gp;
+    size_t gsz;
+    r = d.moduleGetGlobal(&gp, &gsz, m.mod, "lope_tiled_info");
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetGlobal(lope_tiled_info)");
+    int info[4];
+    CUDA_TRY(cudaMemcpy(info, (const void*)gp, sizeof info, cudaMemcpyDeviceToHost));
+    m.tiled_smem = info[0];
+    m.tiled_threads = info[1];
+    m.boxx = info[2];
+    m.boxy = info[3];
+    r = d.funcSetAttribute(m.tiled, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tiled_smem);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuFuncSetAttribute(max dynamic smem)");
+    int nb = 0;
+    r = d.occupancy(&nb, m.tiled, m.tiled_threads, m.tiled_smem);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (nb < 1) return fail(-4, "tiled kernel cannot be resident (smem %d B)", m.tiled_smem);
+    m.tiled_blocks = nb;
+  }
+  K->mods[dev] = m;
+  *out = &K->mods[dev];
+  return 0;
+}
+
+int check_layout(const lope_layout* L) {
+  if (!L) return fail(108, "null layout");
+  if (L->rank < 1 || L->rank > 3) return fail(108, "layout rank %d outside 1..3", L->rank);
+  if (L->dtype != LOPE_F32 && L->dtype != LOPE_F64) return fail(108, "unknown dtype %d", L->dtype);
+  return 0;
+}
+
+template <class T>
+HScal<T> make_scal(const lope::Kir& k, const double* rs, const int64_t* is) {
+  HScal<T> s;
+  std::memset(&s, 0, sizeof s);
+  for (size_t i = 0; i < k.scalars.size(); ++i) {
+    if (k.scalar_is_int[i]) s.v[i] = is ? (T)is[i] : (T)0;
+    else s.v[i] = rs ? (T)rs[i] : (T)0;
+  }
+  return s;
+}
+
+int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtensorMap* map) {
+  cuuint64_t dims[3] = {(cuuint64_t)L->padded[0], (cuuint64_t)L->padded[1], (cuuint64_t)L->padded[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)(L->stride[1] * L->elem_bytes), (cuuint64_t)(L->stride[2] * L->elem_bytes)};
+  cuuint32_t box[3] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = drv().tensorMapEncodeTiled(
+      map, L->dtype == LOPE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
+  return 0;
+}
+
+int zchunk_default(const lope::Kir& k) {
+  if (k.rank < 3) return 1;
+  if (const char* e = std::getenv("LOPE_ZCHUNK")) {
+    int v = std::atoi(e);
+    if (v > 0) return v;
+  }
+  return 16;
+}
+
+// Launch the body kernel over `ranges` (0-based start r0, extents ext) of array set.
+template <class T>
+int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const int ext[3],
+             const void* const* in, void* const* out, const double* rs, const int64_t* is, int wrap,
+             cudaStream_t st) {
+  DevMod* m = nullptr;
+  if (int e = get_mod(K, &m)) return e;
+  const lope::Kir& k = K->ir;
+  HScal<T> sc = make_scal<T>(k, rs, is);
+  HGeom g;
+  std::memset(&g, 0, sizeof g);
+  for (int d = 0; d < 3; ++d) {
+    g.ext[d] = ext[d];
+    g.m[d] = (int)layouts[0].interior[d];
+    g.r0[d] = r0[d];
+    g.lo[d] = layouts[0].lo[d];
+    g.hi[d] = layouts[0].hi[d];
+  }
+  g.wrap = wrap;
+  g.zchunk = zchunk_default(k);
+  Drv& d = drv();
+  const bool use_tiled = K->tiled_ok && k.arrays.size() == 1 && !std::getenv("LOPE_FORCE_GENERIC");
+  if (use_tiled) {
+    const lope_layout* L = &layouts[0];
+    CUtensorMap map;
+    if (int e = encode_tmap(L, in[0], *m, &map)) return e;
+    HArr<T> a;
+    a.in = (const T*)in[0];
+    a.out = (T*)out[0];
+    a.s1 = L->stride[1];
+    a.s2 = L->stride[2];
+    a.org = (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+            (long long)(L->lo[2] + r0[2]) * L->stride[2];
+    const TileCfg& c = K->tile;
+    long long ntx = (ext[0] + 32 * c.bxw - 1) / (32 * c.bxw);
+    long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
+    long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
+    long long units = ntx * nty * nzc;
+    long long grid = (long long)m->tiled_blocks * sm_count();
+    if (const char* e = std::getenv("LOPE_GRID")) grid = std::atoll(e);
+    if (grid > units) grid = units;
+    if (grid < 1) grid = 1;
+    void* args[] = {&map, &a, &sc, &g};
+    CUresult r = d.launchKernel(m->tiled, (unsigned)grid, 1, 1, m->tiled_threads, 1, 1, m->tiled_smem,
+                                (CUstream)st, args, nullptr);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tiled)");
+    g_launches++;
+    return 0;
+  }
+  std::vector<HArr<T>> pack(k.arrays.size());
+  for (size_t i = 0; i < k.arrays.size(); ++i) {
+    const lope_layout* L = &layouts[i];
+    pack[i].in = (const T*)in[i];
+    pack[i].out = out ? (T*)out[i] : nullptr;
+    pack[i].s1 = L->stride[1];
+    pack[i].s2 = L->stride[2];
+    pack[i].org = (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+                  (long long)(L->lo[2] + r0[2]) * L->stride[2];
+  }
+  long long n = (long long)ext[0] * ext[1] * ext[2];
+  long long grid = (n + 255) / 256;
+  long long cap = (long long)sm_count() * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  void* args[] = {pack.data(), &sc, &g};
+  CUresult r = d.launchKernel(m->generic, (unsigned)grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_generic)");
+  g_launches++;
+  return 0;
+}
+
+int row_grid(const lope_layout* L) {
+  long long rows = L->padded[1] * L->padded[2];
+  long long blocks = (rows * 32 + 255) / 256;
+  long long cap = (long long)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+template <class T>
+int copy_through(const lope_layout* L, const void* in, void* out, const int r0[3], const int ext[3],
+                 cudaStream_t st) {
+  DevLayout d = dev_layout(L);
+  int b[3], e[3];
+  for (int i = 0; i < 3; ++i) {
+    b[i] = L->lo[i] + r0[i];
+    e[i] = b[i] + ext[i];
+  }
+  lope_k_copy_through<T><<<row_grid(L), 256, 0, st>>>((const T*)in, (T*)out, d, b[0], e[0], b[1], e[1],
+                                                        b[2], e[2]);
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return 0;
+}
+
+int check_interior_halo(const lope_layout* L) {
+  for (int d = 0; d < L->rank; ++d) {
+    if (L->lo[d] > L->interior[d] || L->hi[d] > L->interior[d])
+      return fail(108, "halo width (%d,%d) exceeds the interior extent %lld in dim %d; the periodic "
+                       "exchange is undefined there (SURVEY F8)",
+                  L->lo[d], L->hi[d], (long long)L->interior[d], d + 1);
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int lope_abi_version(void) { return LOPE_ABI_VERSION; }
+
+const char* lope_last_error(void) { return g_err.c_str(); }
+
+int64_t lope_launch_count(void) { return g_launches.load(); }
+
+int lope_set_cache_dir(const char* path) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_cache_dir = path ? path : "";
+  return 0;
+}
+
+int lope_layout_init(lope_layout* out, int32_t rank, int32_t dtype, const int64_t* interior,
+                     const int32_t* lo, const int32_t* hi) {
+  if (!out || !interior || !lo || !hi) return fail(108, "null argument");
+  if (rank < 1 || rank > 3) return fail(108, "rank %d outside 1..3", rank);
+  if (dtype != LOPE_F32 && dtype != LOPE_F64) return fail(108, "unknown dtype %d", dtype);
+  lope_layout L;
+  std::memset(&L, 0, sizeof L);
+  L.rank = rank;
+  L.dtype = dtype;
+  L.elem_bytes = dtype == LOPE_F32 ? 4 : 8;
+  for (int d = 0; d < 3; ++d) {
+    if (d < rank) {
+      if (interior[d] < 1) return fail(108, "interior extent %lld in dim %d must be positive",
+                                       (long long)interior[d], d + 1);
+      if (interior[d] > (1LL << 30)) return fail(108, "interior extent too large");
+      if (lo[d] < 0 || lo[d] > 8 || hi[d] < 0 || hi[d] > 8)
+        return fail(108, "halo widths (%d,%d) in dim %d outside 0..8", lo[d], hi[d], d + 1);
+      L.interior[d] = interior[d];
+      L.lo[d] = lo[d];
+      L.hi[d] = hi[d];
+    } else {
+      L.interior[d] = 1;
+    }
+    L.padded[d] = L.interior[d] + L.lo[d] + L.hi[d];
+  }
+  const int64_t vec = 16 / L.elem_bytes;
+  L.stride[0] = 1;
+  L.stride[1] = ((L.padded[0] + vec - 1) / vec) * vec;
+  L.stride[2] = L.stride[1] * L.padded[1];
+  L.count = L.stride[2] * L.padded[2];
+  *out = L;
+  return 0;
+}
+
+int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kernel** out) {
+  if (!ir_text || !out) return fail(108, "null argument");
+  if (dtype != LOPE_F32 && dtype != LOPE_F64) return fail(108, "unknown dtype %d", dtype);
+  std::unique_ptr<lope_kernel> K(new lope_kernel());
+  std::string text(ir_text, n);
+  std::string err = lope::parse_kir(text, &K->ir);
+  if (!err.empty()) return fail(104, "kernel IR rejected: %s", err.c_str());
+  K->dtype = dtype;
+  K->tile = pick_tile(K->ir, dtype);
+  K->tiled_ok = K->ir.rank >= 2 && K->ir.arrays.size() == 1 &&
+                tiled_smem_bytes(K->ir, dtype, K->tile) <= 200 * 1024;
+  K->source = build_source(K.get());
+  std::string nm = "lope_" + K->ir.name;
+  if (int e = nvrtc_compile(K->source, nm, &K->cubin)) return e;
+  K->describe_path = K->tiled_ok ? "tiled_tma" : "generic";
+  *out = K.release();
+  return 0;
+}
+
+int lope_kernel_destroy(lope_kernel* k) {
+  if (!k) return 0;
+  Drv& d = drv();
+  for (auto& kv : k->mods)
+    if (kv.second.mod && d.ok) d.moduleUnload(kv.second.mod);
+  delete k;
+  return 0;
+}
+
+int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
+  if (!k || !buf) return fail(108, "null argument");
+  std::ostringstream o;
+  const lope::Kir& ir = k->ir;
+  o << "{\"name\":\"" << ir.name << "\",\"rank\":" << ir.rank << ",\"dtype\":\""
+    << (k->dtype == LOPE_F32 ? "f32" : "f64") << "\",\"arrays\":[";
+  for (size_t i = 0; i < ir.arrays.size(); ++i) o << (i ? "," : "") << "\"" << ir.arrays[i] << "\"";
+  o << "],\"scalars\":[";
+  for (size_t i = 0; i < ir.scalars.size(); ++i)
+    o << (i ? "," : "") << "[\"" << ir.scalars[i] << "\",\"" << (ir.scalar_is_int[i] ? "integer" : "real") << "\"]";
+  o << "],\"stored\":[";
+  for (size_t i = 0; i < ir.stored.size(); ++i) o << (i ? "," : "") << ir.stored[i];
+  o << "],\"footprints\":[";
+  for (size_t a = 0; a < ir.arrays.size(); ++a) {
+    o << (a ? "," : "") << "[";
+    for (int d = 0; d < ir.rank; ++d) o << (d ? "," : "") << "[" << ir.fn[a][d] << "," << ir.fp[a][d] << "]";
+    o << "]";
+  }
+  o << "],\"path\":\"" << k->describe_path << "\",\"tile\":[" << k->tile.bxw << "," << k->tile.wy << ","
+    << k->tile.ry << "," << k->tile.ns << "],\"reads\":" << ir.nreads << "}";
+  std::string s = o.str();
+  if (s.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", s.size() + 1);
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+int lope_kernel_source(const lope_kernel* k, char* buf, size_t n) {
+  if (!k || !buf) return fail(108, "null argument");
+  if (k->source.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", k->source.size() + 1);
+  std::memcpy(buf, k->source.c_str(), k->source.size() + 1);
+  return 0;
+}
+
+int lope_launch(const lope_kernel* kc, const lope_layout* layouts, const int64_t* ranges,
+                const void* const* in, void* const* out, const double* rscal, const int64_t* iscal,
+                void* stream) {
+  lope_kernel* k = const_cast<lope_kernel*>(kc);
+  if (!k || !layouts || !ranges || !in) return fail(108, "null argument");
+  const lope::Kir& ir = k->ir;
+  const int na = (int)ir.arrays.size();
+  for (int a = 0; a < na; ++a) {
+    if (int e = check_layout(&layouts[a])) return e;
+    if (layouts[a].rank != ir.rank)
+      return fail(108, "array '%s' has rank %d, kernel '%s' has rank %d", ir.arrays[a].c_str(),
+                  layouts[a].rank, ir.name.c_str(), ir.rank);
+    if (layouts[a].dtype != k->dtype) return fail(108, "array '%s' dtype differs from the kernel's",
+                                                  ir.arrays[a].c_str());
+    for (int d = 0; d < 3; ++d) {
+      if (layouts[a].interior[d] != layouts[0].interior[d])
+        return fail(108, "array arguments have different interiors");
+      if (ir.fn[a][d] > layouts[a].lo[d] || ir.fp[a][d] > layouts[a].hi[d])
+        return fail(102, "kernel '%s' reads '%s' %d/%d cells out in dim %d but the halo is (%d,%d)",
+                    ir.name.c_str(), ir.arrays[a].c_str(), ir.fn[a][d], ir.fp[a][d], d + 1,
+                    layouts[a].lo[d], layouts[a].hi[d]);
+    }
+    if (!in[a]) return fail(202, "array '%s' is not allocated", ir.arrays[a].c_str());
+  }
+  for (int q : ir.stored) {
+    if (!out || !out[q]) return fail(202, "stored array '%s' has no output buffer", ir.arrays[q].c_str());
+    if (out[q] == in[q]) return fail(108, "output buffer of '%s' aliases its snapshot", ir.arrays[q].c_str());
+  }
+  int r0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+  bool empty = false;
+  for (int d = 0; d < ir.rank; ++d) {
+    int64_t lo = ranges[2 * d], hi = ranges[2 * d + 1];
+    if (lo > hi) {
+      empty = true;
+      continue;
+    }
+    if (lo < 1 || hi > layouts[0].interior[d])
+      return fail(108, "launch range %lld:%lld lies outside the interior 1:%lld in dim %d", (long long)lo,
+                  (long long)hi, (long long)layouts[0].interior[d], d + 1);
+    r0[d] = (int)(lo - 1);
+    ext[d] = (int)(hi - lo + 1);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (empty) {
+    for (int q : ir.stored)
+      CUDA_TRY(cudaMemcpyAsync(out[q], in[q], layouts[q].count * layouts[q].elem_bytes,
+                               cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  int e = k->dtype == LOPE_F32 ? run_body<float>(k, layouts, r0, ext, in, out, rscal, iscal, 0, st)
+                               : run_body<double>(k, layouts, r0, ext, in, out, rscal, iscal, 0, st);
+  if (e) return e;
+  for (int q : ir.stored) {
+    e = k->dtype == LOPE_F32 ? copy_through<float>(&layouts[q], in[q], out[q], r0, ext, st)
+                             : copy_through<double>(&layouts[q], in[q], out[q], r0, ext, st);
+    if (e) return e;
+  }
+  return 0;
+}
+
+int lope_step(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
+              const double* rscal, const int64_t* iscal, int32_t wrap_mask, void* stream) {
+  lope_kernel* k = const_cast<lope_kernel*>(kc);
+  if (!k || !layout) return fail(108, "null argument");
+  if (int e = check_layout(layout)) return e;
+  const lope::Kir& ir = k->ir;
+  if (ir.arrays.size() != 1) return fail(108, "lope_step takes kernels with one array parameter");
+  if (layout->rank != ir.rank || layout->dtype != k->dtype)
+    return fail(108, "layout rank/dtype do not match kernel '%s'", ir.name.c_str());
+  if (!in || !out) return fail(202, "buffer not allocated");
+  if (in == out) return fail(108, "lope_step needs distinct input and output buffers");
+  for (int d = 0; d < 3; ++d)
+    if (ir.fn[0][d] > layout->lo[d] || ir.fp[0][d] > layout->hi[d])
+      return fail(102, "kernel '%s' footprint exceeds the halo in dim %d", ir.name.c_str(), d + 1);
+  if (int e = check_interior_halo(layout)) return e;
+  int r0[3] = {0, 0, 0}, ext[3];
+  for (int d = 0; d < 3; ++d) ext[d] = (int)layout->interior[d];
+  const void* ins[1] = {in};
+  void* outs[1] = {out};
+  int wrap = wrap_mask & ((1 << ir.rank) - 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  return k->dtype == LOPE_F32 ? run_body<float>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st)
+                              : run_body<double>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st);
+}
+
+int lope_halo_fill(const lope_layout* layout, void* buf, int32_t dims_mask, void* stream) {
+  if (int e = check_layout(layout)) return e;
+  if (!buf) return fail(202, "buffer not allocated");
+  if (int e = check_interior_halo(layout)) return e;
+  int mask = dims_mask & ((1 << layout->rank) - 1);
+  bool any = false;
+  for (int d = 0; d < layout->rank; ++d)
+    if ((mask >> d & 1) && (layout->lo[d] || layout->hi[d])) any = true;
+  if (!any) return 0;
+  DevLayout d = dev_layout(layout);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (layout->dtype == LOPE_F32)
+    lope_k_halo_fill<float><<<row_grid(layout), 256, 0, st>>>((float*)buf, d, mask);
+  else
+    lope_k_halo_fill<double><<<row_grid(layout), 256, 0, st>>>((double*)buf, d, mask);
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return 0;
+}
+
+static int pack_impl(const lope_layout* L, const void* host, void* dev, cudaStream_t st, bool to_dev) {
+  if (int e = check_layout(L)) return e;
+  if (!host || !dev) return fail(202, "null buffer");
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof p);
+  const size_t eb = (size_t)L->elem_bytes;
+  cudaPitchedPtr hp = make_cudaPitchedPtr(const_cast<void*>(host), L->interior[0] * eb, L->interior[0],
+                                          L->interior[1]);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, L->stride[1] * eb, L->padded[0], L->padded[1]);
+  cudaPos dpos = make_cudaPos(L->lo[0] * eb, L->lo[1], L->lo[2]);
+  p.extent = make_cudaExtent(L->interior[0] * eb, L->interior[1], L->interior[2]);
+  if (to_dev) {
+    p.srcPtr = hp;
+    p.dstPtr = dp;
+    p.dstPos = dpos;
+    p.kind = cudaMemcpyHostToDevice;
+  } else {
+    p.srcPtr = dp;
+    p.srcPos = dpos;
+    p.dstPtr = hp;
+    p.kind = cudaMemcpyDeviceToHost;
+  }
+  CUDA_TRY(cudaMemcpy3DAsync(&p, st));
+  return 0;
+}
+
+int lope_pack(const lope_layout* layout, const void* host, void* dev, void* stream) {
+  return pack_impl(layout, host, dev, (cudaStream_t)stream, true);
+}
+
+int lope_unpack(const lope_layout* layout, const void* dev, void* host, void* stream) {
+  return pack_impl(layout, host, const_cast<void*>(dev), (cudaStream_t)stream, false);
+}
+
+int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const int64_t* gext,
+                   const int64_t* gorg, void* stream) {
+  if (int e = check_layout(layout)) return e;
+  if (!dev || !gext || !gorg) return fail(202, "null argument");
+  DevLayout d = dev_layout(layout);
+  cudaStream_t st = (cudaStream_t)stream;
+  long long n = layout->interior[0] * layout->interior[1] * layout->interior[2];
+  long long grid = (n + 255) / 256;
+  long long cap = (long long)sm_count() * 16;
+  if (grid > cap) grid = cap;
+  if (layout->dtype == LOPE_F32)
+    lope_k_fill_hash<float><<<(int)grid, 256, 0, st>>>((float*)dev, d, seed, gext[0], gext[1], gorg[0],
+                                                        gorg[1], gorg[2]);
+  else
+    lope_k_fill_hash<double><<<(int)grid, 256, 0, st>>>((double*)dev, d, seed, gext[0], gext[1], gorg[0],
+                                                         gorg[1], gorg[2]);
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return 0;
+}
+
+int lope_face_span(const lope_layout* L, int32_t which, int64_t* offset, int64_t* count) {
+  if (int e = check_layout(L)) return e;
+  if (!offset || !count) return fail(108, "null argument");
+  const int d = L->rank - 1;
+  const int64_t plane = d == 0 ? 1 : L->stride[d];
+  const int64_t m = L->interior[d];
+  const int lo = L->lo[d], hi = L->hi[d];
+  switch (which) {
+    case 0: *offset = 0; *count = lo * plane; break;                       // low halo
+    case 1: *offset = (lo + m) * plane; *count = hi * plane; break;        // high halo
+    case 2: *offset = lo * plane; *count = hi * plane; break;              // first `hi` interior planes
+    case 3: *offset = m * plane; *count = lo * plane; break;               // last `lo` interior planes
+    default: return fail(108, "face selector %d outside 0..3", which);
+  }
+  return 0;
+}
+
+}  // extern "C"

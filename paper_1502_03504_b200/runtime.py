@@ -1,0 +1,310 @@
+"""Host runtime: GPU-resident halo arrays, kernel launches and halo transfers.
+
+This is the reference's hot path (lopec/runtime.py) re-expressed over
+liblope_b200.so.  Vocabulary and semantics follow the reference:
+
+* ``HaloArray`` — one image's block of a halo-padded array
+  (``DistributedArray`` blocks, runtime.py:73-94; layout ir.py:189-230), kept in
+  HBM.  It owns two buffers: the live one and a spare that becomes the next
+  launch's output (the double buffering of ``_launch``: the reference copies a
+  snapshot, runtime.py:596; here the live buffer *is* the snapshot and the
+  spare receives the stores, so no copy is made).
+* ``launch``   — ``Machine._launch`` + ``_launch_vector`` (runtime.py:541-618):
+  1-based inclusive ranges, E108 outside the interior, empty ranges allowed.
+* ``halo_transfer`` — ``Machine._halo_exchange`` (runtime.py:643-711) for an
+  image that is its own neighbour in every dimension (P = 1).  Partitioned
+  arrays use ``paper_1502_03504_b200.dist``.
+* ``iterate``  — ``do it = 1, nsteps; HALO_TRANSFER(U); do concurrent ... end
+  do`` (corpus/*.lope).  Steps 1..K-1 run as one fused kernel each (launch of
+  step t + the periodic fill of step t+1); the last launch copies the halo
+  through, so the final state equals the reference's.
+
+Buffers are torch CUDA tensors (torch is used for allocation, streams and
+copies only); every computation is a liblope_b200.so kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .diagnostics import ALLOC_SHAPE, RuntimeFault
+from .ir import KernelIR, deserialize, serialize
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _torch_dtype(code):
+    torch = _torch()
+    return torch.float32 if code == _lib.F32 else torch.float64
+
+
+def _np_dtype(code):
+    return np.float32 if code == _lib.F32 else np.float64
+
+
+class HaloArray:
+    """A halo-padded array block resident in HBM (``real, dimension(...), HALO(lo:*:hi, ...)``).
+
+    ``interior``: extents m_d; ``lo``/``hi``: halo widths per dim (0..8).
+    """
+
+    def __init__(self, interior: Sequence[int], lo: Sequence[int], hi: Sequence[int],
+                 dtype="float32", device=None, name: str = "u"):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("HaloArray needs a CUDA device (there is no CPU path)")
+        interior = tuple(int(m) for m in interior)
+        rank = len(interior)
+        if len(lo) != rank or len(hi) != rank:
+            raise RuntimeFault(ALLOC_SHAPE, "halo widths must have one entry per dimension")
+        self.name = name
+        self.rank = rank
+        self.interior = interior
+        self.lo = tuple(int(w) for w in lo)
+        self.hi = tuple(int(w) for w in hi)
+        self.layout = _lib.make_layout(rank, dtype, interior, self.lo, self.hi)
+        self.dtype_code = self.layout.dtype
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self._bufs = [torch.zeros(self.layout.count, dtype=_torch_dtype(self.dtype_code),
+                                  device=self.device), None]
+        self._live = 0
+
+    # -- buffers -----------------------------------------------------------
+
+    @property
+    def data(self):
+        """The live buffer (flat, ``layout.count`` elements)."""
+        return self._bufs[self._live]
+
+    def spare(self):
+        """The other buffer of the ping-pong pair (allocated on first use)."""
+        torch = _torch()
+        j = 1 - self._live
+        if self._bufs[j] is None:
+            self._bufs[j] = torch.zeros_like(self._bufs[self._live])
+        return self._bufs[j]
+
+    def swap(self) -> None:
+        self._live = 1 - self._live
+
+    def padded_view(self):
+        """Device view of the padded block as a torch tensor indexed [c2, c1, c0]."""
+        L = self.layout
+        p = [int(L.padded[d]) for d in range(3)]
+        v = self.data.view(p[2], p[1], int(L.stride[1]))
+        return v[:, :, :p[0]]
+
+    def interior_view(self):
+        L = self.layout
+        v = self.padded_view()
+        return v[L.lo[2]:L.lo[2] + L.interior[2], L.lo[1]:L.lo[1] + L.interior[1],
+                 L.lo[0]:L.lo[0] + L.interior[0]]
+
+    # -- host transfers (scatter / gather) ----------------------------------
+
+    def set_interior(self, field: np.ndarray, stream=None) -> None:
+        """``_scatter_block`` (runtime.py:477-486): host field -> interior."""
+        field = np.asarray(field, dtype=_np_dtype(self.dtype_code))
+        if field.shape != self.interior:
+            raise RuntimeFault(ALLOC_SHAPE, f"field shape {field.shape} does not match the "
+                                            f"interior {self.interior}")
+        host = np.asfortranarray(field)
+        _lib.check(_lib.lib().lope_pack(ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.c_void_p(self.data.data_ptr()),
+                                        ctypes.c_void_p(_stream_handle(stream))), "lope_pack")
+        _torch().cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+
+    def upload(self, host_ptr: int, stream=None) -> None:
+        """Interior <- host column-major buffer at ``host_ptr`` (pinned for async copies)."""
+        _lib.check(_lib.lib().lope_pack(ctypes.byref(self.layout), ctypes.c_void_p(host_ptr),
+                                        ctypes.c_void_p(self.data.data_ptr()),
+                                        ctypes.c_void_p(_stream_handle(stream))), "lope_pack")
+
+    def download(self, host_ptr: int, stream=None) -> None:
+        """Host column-major buffer at ``host_ptr`` <- interior (asynchronous on the stream)."""
+        _lib.check(_lib.lib().lope_unpack(ctypes.byref(self.layout), ctypes.c_void_p(self.data.data_ptr()),
+                                          ctypes.c_void_p(host_ptr),
+                                          ctypes.c_void_p(_stream_handle(stream))), "lope_unpack")
+
+    def get_interior(self, stream=None) -> np.ndarray:
+        """Gather the interior to the host (numpy, reference index order)."""
+        out = np.empty(self.interior, dtype=_np_dtype(self.dtype_code), order="F")
+        _lib.check(_lib.lib().lope_unpack(ctypes.byref(self.layout),
+                                          ctypes.c_void_p(self.data.data_ptr()),
+                                          out.ctypes.data_as(ctypes.c_void_p),
+                                          ctypes.c_void_p(_stream_handle(stream))), "lope_unpack")
+        _torch().cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        return np.ascontiguousarray(out) if out.ndim == 1 else out
+
+    def get_padded(self) -> np.ndarray:
+        """The whole padded block on the host, numpy index order (c0, c1, ...)."""
+        v = self.padded_view().cpu().numpy()          # [c2, c1, c0]
+        v = np.transpose(v, (2, 1, 0))
+        return np.ascontiguousarray(v.reshape(v.shape[:self.rank]))
+
+    def fill_hash(self, seed: int, global_extent=None, global_origin=None, stream=None) -> None:
+        """Synthetic U(-1,1) field generated on the device (oracle: hash_values)."""
+        ge = list(global_extent or self.interior) + [1] * (3 - len(global_extent or self.interior))
+        go = list(global_origin or [0] * self.rank) + [0] * (3 - len(global_origin or [0] * self.rank))
+        _lib.check(_lib.lib().lope_fill_hash(ctypes.byref(self.layout),
+                                             ctypes.c_void_p(self.data.data_ptr()),
+                                             ctypes.c_uint64(seed), (ctypes.c_int64 * 3)(*ge),
+                                             (ctypes.c_int64 * 3)(*go),
+                                             ctypes.c_void_p(_stream_handle(stream))),
+                   "lope_fill_hash")
+
+    def nbytes_interior(self) -> int:
+        return int(np.prod(self.interior)) * int(self.layout.elem_bytes)
+
+
+class CompiledKernel:
+    """A locally-oriented kernel compiled for sm_100a (``lope_kernel_compile``)."""
+
+    def __init__(self, kernel, dtype="float32"):
+        if isinstance(kernel, KernelIR):
+            self.ir = kernel
+            text = serialize(kernel)
+        elif isinstance(kernel, str):
+            text = kernel
+            self.ir = deserialize(text)
+        else:      # a lopec.ir.KernelIR (duck-typed)
+            from .ir import from_lopec
+            self.ir = from_lopec(kernel)
+            text = serialize(self.ir)
+        self.text = text
+        self.dtype_code = _lib.dtype_code(dtype)
+        self.handle = _lib.compile_kernel(text, self.dtype_code)
+
+    def __del__(self):
+        try:
+            _lib.destroy_kernel(getattr(self, "handle", None))
+        except Exception:
+            pass
+
+    def describe(self) -> str:
+        return _lib.describe(self.handle)
+
+    def source(self) -> str:
+        return _lib.source(self.handle)
+
+    def scalar_args(self, scalars: Optional[Dict[str, float]]):
+        scalars = scalars or {}
+        n = max(1, len(self.ir.scalar_params))
+        rs = (ctypes.c_double * n)()
+        is_ = (ctypes.c_int64 * n)()
+        for i, name in enumerate(self.ir.scalar_params):
+            if name not in scalars:
+                raise RuntimeFault("E202", f"scalar parameter '{name}' has no value")
+            v = scalars[name]
+            if self.ir.param_types.get(name) == "integer":
+                is_[i] = int(v)
+            else:
+                rs[i] = float(v)
+        return rs, is_
+
+
+def launch(kernel: CompiledKernel, arrays: Sequence[HaloArray], ranges=None,
+           scalars: Optional[Dict[str, float]] = None, stream=None) -> None:
+    """One ``do concurrent`` launch (runtime.py:541-618) over 1-based inclusive ``ranges``.
+
+    ``arrays`` binds the kernel's array parameters in order.  Stored arrays are
+    written into their spare buffer (the reference's live buffer) and become
+    live; everything outside the range is copied through.
+    """
+    ir = kernel.ir
+    if len(arrays) != len(ir.array_params):
+        raise RuntimeFault(ALLOC_SHAPE, f"kernel '{ir.name}' takes {len(ir.array_params)} arrays")
+    if len({id(a) for a in arrays}) != len(arrays):
+        raise RuntimeFault(ALLOC_SHAPE, "the same array is bound to two kernel parameters")
+    rank = ir.rank
+    if ranges is None:
+        ranges = [(1, m) for m in arrays[0].interior]
+    if len(ranges) != rank:
+        raise RuntimeFault(ALLOC_SHAPE, f"launch needs {rank} ranges")
+    na = len(arrays)
+    layouts = (_lib.Layout * na)(*[a.layout for a in arrays])
+    rng = (ctypes.c_int64 * (2 * rank))(*[int(v) for r in ranges for v in r])
+    ins = (ctypes.c_void_p * na)(*[a.data.data_ptr() for a in arrays])
+    stored = set(ir.stored_arrays)
+    outs = (ctypes.c_void_p * na)(*[(a.spare().data_ptr() if p in stored else None)
+                                    for p, a in zip(ir.array_params, arrays)])
+    rs, is_ = kernel.scalar_args(scalars)
+    _lib.check(_lib.lib().lope_launch(kernel.handle, layouts, rng, ins, outs, rs, is_,
+                                      ctypes.c_void_p(_stream_handle(stream))), "lope_launch")
+    for p, a in zip(ir.array_params, arrays):
+        if p in stored:
+            a.swap()
+
+
+def halo_transfer(arr: HaloArray, dims_mask: Optional[int] = None, stream=None) -> None:
+    """``HALO_TRANSFER(U, BC=CYCLIC)`` for one image (every neighbour is self)."""
+    mask = (1 << arr.rank) - 1 if dims_mask is None else dims_mask
+    _lib.check(_lib.lib().lope_halo_fill(ctypes.byref(arr.layout), ctypes.c_void_p(arr.data.data_ptr()),
+                                         mask, ctypes.c_void_p(_stream_handle(stream))),
+               "lope_halo_fill")
+
+
+def step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Optional[int] = None,
+         stream=None) -> None:
+    """Fused launch (full interior) + the following HALO_TRANSFER's local fill."""
+    mask = (1 << arr.rank) - 1 if wrap_mask is None else wrap_mask
+    rs, is_ = kernel.scalar_args(scalars)
+    _lib.check(_lib.lib().lope_step(kernel.handle, ctypes.byref(arr.layout),
+                                    ctypes.c_void_p(arr.data.data_ptr()),
+                                    ctypes.c_void_p(arr.spare().data_ptr()), rs, is_, mask,
+                                    ctypes.c_void_p(_stream_handle(stream))), "lope_step")
+    arr.swap()
+
+
+def iterate(kernel: CompiledKernel, arr: HaloArray, steps: int, scalars=None, stream=None) -> None:
+    """``do it = 1, steps; HALO_TRANSFER(U); do concurrent (full interior) call K(U); end do``."""
+    if steps <= 0:
+        return
+    halo_transfer(arr, stream=stream)
+    for _ in range(steps - 1):
+        step(kernel, arr, scalars, stream=stream)
+    launch(kernel, [arr], None, scalars, stream=stream)
+
+
+def run(kernel, field: np.ndarray, steps: int, scalars=None, halo=None, dtype=None) -> np.ndarray:
+    """End-to-end: host field in, ``steps`` iterations on the GPU, host field out."""
+    if not isinstance(kernel, CompiledKernel):
+        kernel = CompiledKernel(kernel, dtype or "float32")
+    ir = kernel.ir
+    fp = ir.footprints[ir.array_params[0]].dims
+    lo = [n for n, _ in fp] if halo is None else [h[0] for h in halo]
+    hi = [p for _, p in fp] if halo is None else [h[1] for h in halo]
+    field = np.asarray(field)
+    arr = HaloArray(field.shape, lo, hi, dtype="float32" if kernel.dtype_code == _lib.F32 else "float64")
+    arr.set_interior(field)
+    iterate(kernel, arr, steps, scalars)
+    return arr.get_interior()
+
+
+def run_pinned(kernel: CompiledKernel, shape, lo, hi, dtype, host_in, host_out, steps: int,
+               scalars=None, stream=None) -> None:
+    """End-to-end through the public API with caller-provided (pinned) host buffers.
+
+    ``host_in`` / ``host_out``: torch CPU tensors holding the interior in
+    column-major order (numpy ``order='F'``).  Returns after the download
+    has completed.
+    """
+    arr = HaloArray(shape, lo, hi, dtype)
+    arr.upload(host_in.data_ptr(), stream)
+    iterate(kernel, arr, steps, scalars, stream)
+    arr.download(host_out.data_ptr(), stream)
+    (stream or _torch().cuda.current_stream()).synchronize()

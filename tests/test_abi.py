@@ -1,0 +1,92 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the header
+declares, lays out blocks as the reference does, compiles kernels (NVRTC needs no
+GPU) and rejects bad input with the reference's error codes.  No kernel runs here."""
+
+import json
+import re
+
+import pytest
+
+from conftest import REPO
+from paper_1502_03504_b200 import _lib, stencils
+from paper_1502_03504_b200.diagnostics import RuntimeFault
+from paper_1502_03504_b200.ir import KernelBuilder, serialize
+
+
+def header_symbols():
+    text = (REPO / "include" / "lope_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(lope_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert L.lope_abi_version() == 1
+
+
+def test_layout_matches_reference_storage_layout():
+    # StorageLayout((8,4,3),(1,2,0),(1,0,1)): padded (10,6,4) (tests/test_layout.py:24-29)
+    L = _lib.make_layout(3, "f32", (8, 4, 3), (1, 2, 0), (1, 0, 1))
+    assert tuple(L.padded) == (10, 6, 4)
+    # row pitch rounded to 16 bytes for TMA; otherwise column-major like the reference
+    assert L.stride[0] == 1 and L.stride[1] == 12 and L.stride[2] == 12 * 6
+    assert L.count == 12 * 6 * 4
+    # frozen KAT (test_layout.py:14-21): 8x4 interior, halo 1, centre (1,1)+(1,0) -> coords (2,1)
+    L2 = _lib.make_layout(2, "f64", (8, 4), (1, 1), (1, 1))
+    assert L2.stride[1] == 10      # 10 doubles = 80 B, already a 16 B multiple
+    assert 2 + 1 * L2.stride[1] == 12
+    assert 9 + 5 * L2.stride[1] == 59
+
+
+def test_layout_rejects_bad_shapes():
+    with pytest.raises(RuntimeFault) as e:
+        _lib.make_layout(2, "f32", (0, 4), (1, 1), (1, 1))
+    assert e.value.code == "E108"
+    with pytest.raises(RuntimeFault) as e:
+        _lib.make_layout(2, "f32", (4, 4), (9, 1), (1, 1))
+    assert e.value.code == "E108"
+
+
+def test_face_spans_are_contiguous_planes():
+    L = _lib.make_layout(3, "f32", (8, 6, 10), (1, 1, 2), (1, 1, 1))
+    plane = L.stride[2]
+    assert _lib.face_span(L, 0) == (0, 2 * plane)
+    assert _lib.face_span(L, 1) == ((2 + 10) * plane, 1 * plane)
+    assert _lib.face_span(L, 2) == (2 * plane, 1 * plane)
+    assert _lib.face_span(L, 3) == (10 * plane, 2 * plane)
+
+
+def test_kernels_compile_and_describe():
+    for name in ("lap3d7", "ninept2d", "box5x5", "drift2", "avg3"):
+        h = _lib.compile_kernel(serialize(stencils.by_name(name)), "f32")
+        d = json.loads(_lib.describe(h))
+        assert d["name"] == name
+        if name in ("lap3d7", "ninept2d", "box5x5", "drift2"):
+            assert d["path"] == "tiled_tma"
+        else:
+            assert d["path"] == "generic"
+        src = _lib.source(h)
+        assert "__fadd_rn" in src and "cp.async.bulk.tensor" in src
+        _lib.destroy_kernel(h)
+
+
+def test_constants_cross_the_boundary_exactly():
+    k = KernelBuilder("c", 2)
+    u = k.array("u")
+    k.store(u, u[0, 0] * 0.1 + 1e-300)
+    h = _lib.compile_kernel(serialize(k.build()), "f64")
+    src = _lib.source(h)
+    assert "T(" + (0.1).hex().replace("0x1.", "0x1.") in src or "0x1.999999999999ap-4" in src
+    _lib.destroy_kernel(h)
+
+
+def test_bad_ir_is_rejected():
+    with pytest.raises(RuntimeFault) as e:
+        _lib.compile_kernel("LOPE1\nkernel k 2\narray u\nstore u r v 0 0\nend\n", "f32")
+    assert e.value.code == "E104"
+    with pytest.raises(RuntimeFault):
+        _lib.compile_kernel("LOPE1\nkernel k 2\narray u\nstore u r u 0 0\nstore u r u 1 0\nend\n", "f32")

@@ -1,0 +1,263 @@
+"""GPU parity: liblope_b200.so kernels against the reference's golden outputs and the oracle.
+
+fp64 runs must equal the reference ``Machine`` / ``oracle_step`` outputs bit for
+bit (tests/golden, generated from the reference).  fp32 runs must equal the
+fp32 restatement (oracle/lope_oracle.py) bit for bit — NaN payloads excepted
+(every NaN compares equal).  All calls go through the C ABI.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lope_oracle as O
+from paper_1502_03504_b200 import stencils
+from paper_1502_03504_b200.diagnostics import RuntimeFault
+from paper_1502_03504_b200.ir import deserialize
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1502_03504_b200 import runtime as R  # noqa: E402
+
+_KCACHE = {}
+
+
+def K(kir, dtype):
+    key = (id(kir) if not isinstance(kir, str) else kir, dtype)
+    if isinstance(kir, str):
+        kir = deserialize(kir)
+    name = (kir.name, dtype, repr(kir.body))
+    if name not in _KCACHE:
+        _KCACHE[name] = R.CompiledKernel(kir, dtype)
+    return _KCACHE[name]
+
+
+def halos_of(kir):
+    fp = kir.footprints[kir.array_params[0]].dims
+    return [n for n, _ in fp], [p for _, p in fp]
+
+
+def gpu_iterate(kir, field, steps, scalars, dtype, lo=None, hi=None):
+    l_, h_ = halos_of(kir)
+    lo = l_ if lo is None else lo
+    hi = h_ if hi is None else hi
+    arr = R.HaloArray(field.shape, lo, hi, dtype)
+    arr.set_interior(field)
+    R.iterate(K(kir, dtype), arr, steps, scalars)
+    return arr
+
+
+def test_fp64_matches_reference_machine_bitwise(golden_runs):
+    index, arrs = golden_runs
+    for case in index:
+        kir = stencils.by_name(case["kernel"])
+        field = arrs[case["tag"] + "_in"]
+        arr = gpu_iterate(kir, field, case["steps"], case["scalars"], "float64")
+        got = arr.get_interior()
+        assert O.equal_bits(got, arrs[case["tag"] + "_out"]), (case["tag"], O.first_mismatch(
+            got, arrs[case["tag"] + "_out"]))
+
+
+def test_fp32_matches_restatement_bitwise(golden_runs):
+    index, arrs = golden_runs
+    for case in index:
+        kir = stencils.by_name(case["kernel"])
+        field = arrs[case["tag"] + "_in"].astype(np.float32)
+        got = gpu_iterate(kir, field, case["steps"], case["scalars"], "float32").get_interior()
+        want = field
+        for _ in range(case["steps"]):
+            want = O.periodic_apply(want, kir, case["scalars"], np.float32)
+        assert O.equal_bits(got, want), (case["tag"], O.first_mismatch(got, want))
+
+
+def test_final_halo_state_matches_reference_machine():
+    """After iterate(), halo cells hold the last exchange's values, as in the reference."""
+    kir = stencils.heat2d()
+    field = O.hash_field((24, 20), 9, np.float64)
+    arr = gpu_iterate(kir, field, 4, {}, "float64")
+    want = O.machine_run(field, kir, 4, None, np.float64)
+    assert O.equal_bits(arr.get_padded(), want)
+
+
+def test_random_kernels_fp64_and_fp32(golden_random):
+    meta, arrs = golden_random
+    for m in meta:
+        kir = deserialize(m["ir"])
+        field = arrs[f"r{m['trial']}_in"]
+        for dtype, npdt in (("float64", np.float64), ("float32", np.float32)):
+            f = field.astype(npdt)
+            arr = gpu_iterate(kir, f, 1, m["scalars"], dtype, lo=[2] * kir.rank, hi=[2] * kir.rank)
+            got = arr.get_interior()
+            if npdt == np.float64:
+                want = arrs[f"r{m['trial']}_out"]
+            else:
+                want = O.periodic_apply(f, kir, m["scalars"], np.float32)
+            assert O.equal_bits(got, want), (m["trial"], dtype, m["source"], O.first_mismatch(got, want))
+
+
+def test_generic_and_tiled_paths_agree(monkeypatch):
+    for name, shape, dt in (("lap3d7", (70, 37, 19), "float32"), ("box5x5", (150, 67), "float64"),
+                            ("ninept2d", (131, 45), "float32"), ("drift2", (77, 41), "float32")):
+        kir = stencils.by_name(name)
+        f = O.hash_field(shape, 3, np.float32 if dt == "float32" else np.float64)
+        sc = {"c": 0.25} if name == "drift2" else {}
+        a = gpu_iterate(kir, f, 3, sc, dt).get_padded()
+        monkeypatch.setenv("LOPE_FORCE_GENERIC", "1")
+        b = gpu_iterate(kir, f, 3, sc, dt).get_padded()
+        monkeypatch.delenv("LOPE_FORCE_GENERIC")
+        assert O.equal_bits(a, b), name
+
+
+def test_tile_schedule_order_invariance(monkeypatch):
+    """The --shuffle-seed analogue: different CTA->unit mappings give identical bits."""
+    kir = stencils.lap3d7()
+    f = O.hash_field((96, 40, 33), 8, np.float32)
+    base = gpu_iterate(kir, f, 2, {}, "float32").get_interior()
+    for grid, zc in (("1", "16"), ("7", "5"), ("293", "1"), ("5000", "64")):
+        monkeypatch.setenv("LOPE_GRID", grid)
+        monkeypatch.setenv("LOPE_ZCHUNK", zc)
+        got = gpu_iterate(kir, f, 2, {}, "float32").get_interior()
+        assert O.equal_bits(got, base), (grid, zc)
+
+
+def test_halo_transfer_fills_every_padded_cell(golden_exchange):
+    index, arrs = golden_exchange
+    for case in index:
+        if case["p"] != 1:
+            continue
+        l0, h0, l1, h1 = case["widths"]
+        field = arrs[case["tag"] + "_in"]
+        arr = R.HaloArray(field.shape, (l0, l1), (h0, h1), "float64")
+        arr.set_interior(field)
+        R.halo_transfer(arr)
+        assert np.array_equal(arr.get_padded(), arrs[case["tag"] + "_blk1"]), case["tag"]
+
+
+def test_subrange_launch_copies_through(golden_kats):
+    kir = deserialize(golden_kats["subrange_ir"])
+    f = np.array(golden_kats["subrange_in"])
+    arr = R.HaloArray(f.shape, (1, 1), (1, 1), "float64")
+    arr.set_interior(f)
+    k = K(kir, "float64")
+    for _ in range(3):
+        R.halo_transfer(arr)
+        R.launch(k, [arr], [(2, f.shape[0] - 1), (3, f.shape[1])])
+    assert np.array_equal(arr.get_padded(), np.array(golden_kats["subrange_out_padded"]))
+
+
+def test_two_array_kernel_and_pending_centre(golden_kats):
+    kir = deserialize(golden_kats["mix_ir"])
+    f = np.array(golden_kats["mix_in"])
+    u = R.HaloArray(f.shape, (1, 1), (1, 1), "float64", name="u")
+    v = R.HaloArray(f.shape, (1, 1), (1, 1), "float64", name="v")
+    u.set_interior(f)
+    v.set_interior(f)
+    k = K(kir, "float64")
+    for _ in range(4):
+        R.halo_transfer(u)
+        R.halo_transfer(v)
+        R.launch(k, [u, v])
+    assert np.array_equal(u.get_padded(), np.array(golden_kats["mix_out_u"]))
+    assert np.array_equal(v.get_padded(), np.array(golden_kats["mix_out_v"]))
+    twice = deserialize(golden_kats["twice_ir"])
+    g = np.full((4, 4), 1.5)
+    arr = R.HaloArray(g.shape, (1, 1), (1, 1), "float64")
+    arr.set_interior(g)
+    R.launch(K(twice, "float64"), [arr])
+    assert np.array_equal(arr.get_interior(), g * 2 + 1)
+
+
+def test_point_source_and_fixed_point_kats(golden_kats):
+    kir = stencils.laplacian()
+    f = np.zeros((4, 4)); f[1, 1] = 1.0
+    assert np.array_equal(R.run(kir, f, 1, dtype="float64"), np.array(golden_kats["point_source"]))
+    f = np.zeros((4, 4)); f[0, 0] = 1.0
+    assert np.array_equal(R.run(kir, f, 1, dtype="float64"), np.array(golden_kats["corner_source"]))
+    ones = np.full((8, 8), 1.0)
+    assert np.array_equal(R.run(kir, ones, 25, dtype="float64"), ones)
+
+
+def test_empty_range_and_faults():
+    kir = stencils.heat2d()
+    f = O.hash_field((8, 8), 1, np.float64)
+    arr = R.HaloArray(f.shape, (1, 1), (1, 1), "float64")
+    arr.set_interior(f)
+    k = K(kir, "float64")
+    R.launch(k, [arr], [(1, 0), (1, 8)])
+    assert np.array_equal(arr.get_interior(), f)
+    with pytest.raises(RuntimeFault) as e:
+        R.launch(k, [arr], [(1, 9), (1, 8)])
+    assert e.value.code == "E108"
+    thin = R.HaloArray((8, 8), (0, 1), (1, 1), "float64")
+    with pytest.raises(RuntimeFault) as e:
+        R.launch(k, [thin])
+    assert e.value.code == "E102"
+    narrow = R.HaloArray((1, 8), (2, 1), (2, 1), "float64")      # halo wider than interior (F8)
+    with pytest.raises(RuntimeFault) as e:
+        R.halo_transfer(narrow)
+    assert e.value.code == "E108"
+
+
+def test_device_hash_fill_matches_oracle():
+    for dt, npdt in (("float32", np.float32), ("float64", np.float64)):
+        arr = R.HaloArray((33, 17, 9), (1, 1, 1), (1, 1, 1), dt)
+        arr.fill_hash(1234)
+        assert O.equal_bits(arr.get_interior(), O.hash_field((33, 17, 9), 1234, npdt))
+        arr = R.HaloArray((20, 12), (2, 2), (2, 2), dt)
+        arr.fill_hash(77, global_extent=(20, 48), global_origin=(0, 24))
+        assert O.equal_bits(arr.get_interior(), O.hash_field((20, 48), 77, npdt)[:, 24:36])
+
+
+def _planes_check(arr, kir, gshape, seed, npdt, planes, steps_done=1):
+    assert steps_done == 1
+    L = arr.layout
+    v = arr.interior_view()            # [c2, c1, c0]
+    for z0, z1 in planes:
+        got = v[z0:z1].cpu().numpy().transpose(2, 1, 0) if arr.rank == 3 else None
+        if arr.rank == 2:
+            got = v[0, z0:z1, :].cpu().numpy().transpose(1, 0)
+        want = O.periodic_apply_planes(lambda idx: O.hash_planes(gshape, seed, idx, npdt), gshape,
+                                       kir, z0, z1, None, npdt)
+        assert O.equal_bits(got, want), (z0, z1, O.first_mismatch(got, want))
+
+
+@pytest.mark.parametrize("name,shape,dt", [
+    ("lap3d7", (1024, 1024, 1024), "float32"),
+    ("ninept2d", (16384, 16384), "float32"),
+    ("box5x5", (32768, 32768), "float64"),
+])
+def test_full_size_one_step_sampled_planes(name, shape, dt):
+    """BASELINE sizes: device-generated input, one step, sampled planes vs the oracle."""
+    kir = stencils.by_name(name)
+    npdt = np.float32 if dt == "float32" else np.float64
+    lo, hi = halos_of(kir)
+    arr = R.HaloArray(shape, lo, hi, dt)
+    arr.fill_hash(20260823)
+    R.iterate(K(kir, dt), arr, 1)
+    n = shape[-1]
+    _planes_check(arr, kir, shape, 20260823, npdt, [(0, 2), (n // 2 - 1, n // 2 + 1), (n - 2, n)])
+    del arr
+    torch.cuda.empty_cache()
+
+
+def test_full_size_multi_step_tiled_equals_generic(monkeypatch):
+    """Config 3 at full size, 5 steps: TMA tiled path == independent generic path, bit for bit."""
+    kir = stencils.lap3d7()
+    shape = (1024, 1024, 1024)
+    a = R.HaloArray(shape, (1, 1, 1), (1, 1, 1), "float32")
+    a.fill_hash(5)
+    R.iterate(K(kir, "float32"), a, 5)
+    monkeypatch.setenv("LOPE_FORCE_GENERIC", "1")
+    b = R.HaloArray(shape, (1, 1, 1), (1, 1, 1), "float32")
+    b.fill_hash(5)
+    R.iterate(K(kir, "float32"), b, 5)
+    assert torch.equal(a.padded_view().contiguous().view(torch.int32),
+                       b.padded_view().contiguous().view(torch.int32))
+    del a, b
+    torch.cuda.empty_cache()
