@@ -42,9 +42,11 @@ extern "C" {
 #define LOPE_F64 2
 
 /* Device storage of one image's block: the reference's padded column-major block
- * (ir.py:189-230: padded_d = m_d + lo_d + hi_d, dim 1 fastest) with the row pitch
- * rounded up to 16 bytes (TMA stride rule).  Element at 0-based padded
- * coordinates (c0,c1,c2) is at c0 + c1*stride[1] + c2*stride[2]. */
+ * (ir.py:189-230: padded_d = m_d + lo_d + hi_d, dim 1 fastest) with every row
+ * shifted so its first interior element sits on a 128-byte boundary and the row
+ * pitch a multiple of 128 bytes (whole-line warp stores; 16-byte TMA strides).
+ * Element at 0-based padded coordinates (c0,c1,c2) is at
+ * base + c0 + c1*stride[1] + c2*stride[2]. */
 typedef struct lope_layout {
   int32_t rank;          /* 1..3 */
   int32_t dtype;         /* LOPE_F32 | LOPE_F64 */
@@ -55,6 +57,7 @@ typedef struct lope_layout {
   int64_t stride[3];     /* element strides: 1, row pitch, plane pitch */
   int64_t count;         /* elements to allocate */
   int64_t elem_bytes;
+  int64_t base;          /* element offset of padded cell (0,0,0) */
 } lope_layout;
 
 typedef struct lope_kernel lope_kernel;

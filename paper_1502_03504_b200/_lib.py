@@ -30,7 +30,7 @@ class Layout(ctypes.Structure):
                 ("interior", ctypes.c_int64 * 3), ("lo", ctypes.c_int32 * 3),
                 ("hi", ctypes.c_int32 * 3), ("padded", ctypes.c_int64 * 3),
                 ("stride", ctypes.c_int64 * 3), ("count", ctypes.c_int64),
-                ("elem_bytes", ctypes.c_int64)]
+                ("elem_bytes", ctypes.c_int64), ("base", ctypes.c_int64)]
 
     def __repr__(self):
         r = self.rank
@@ -95,6 +95,8 @@ def check(rc: int, what: str) -> None:
 
 def dtype_code(dtype) -> int:
     import numpy as np
+    if isinstance(dtype, int) and dtype in (F32, F64):
+        return dtype
     if isinstance(dtype, str) and dtype in DTYPES:
         return DTYPES[dtype]
     dt = np.dtype(str(dtype).replace("torch.", ""))

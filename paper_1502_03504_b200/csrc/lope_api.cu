@@ -114,7 +114,7 @@ struct DevLayout {
   int rank;
   int m[3], lo[3], hi[3];
   long long P[3];
-  long long S1, S2;
+  long long S1, S2, B;
 };
 
 DevLayout dev_layout(const lope_layout* L) {
@@ -128,6 +128,7 @@ DevLayout dev_layout(const lope_layout* L) {
   }
   d.S1 = L->stride[1];
   d.S2 = L->stride[2];
+  d.B = L->base;
   return d;
 }
 
@@ -167,8 +168,8 @@ __global__ void __launch_bounds__(256) lope_k_halo_fill(T* __restrict__ buf, Dev
     const int c2 = (int)(r / L.P[1]);
     const int s1 = (mask & 2) ? lope_wrapc(c1, L.lo[1], L.m[1]) : c1;
     const int s2 = (mask & 4) ? lope_wrapc(c2, L.lo[2], L.m[2]) : c2;
-    T* dst = buf + c1 * L.S1 + c2 * L.S2;
-    const T* src = buf + s1 * L.S1 + s2 * L.S2;
+    T* dst = buf + L.B + c1 * L.S1 + c2 * L.S2;
+    const T* src = buf + L.B + s1 * L.S1 + s2 * L.S2;
     if (s1 != c1 || s2 != c2) {
       for (int x = lane; x < L.P[0]; x += 32)
         dst[x] = src[(mask & 1) ? lope_wrapc(x, L.lo[0], L.m[0]) : x];
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(256) lope_k_copy_through(const T* __restrict__
   for (long long r = warp; r < nrows; r += nw) {
     const int c1 = (int)(r % L.P[1]);
     const int c2 = (int)(r / L.P[1]);
-    const long long base = c1 * L.S1 + c2 * L.S2;
+    const long long base = L.B + c1 * L.S1 + c2 * L.S2;
     const bool inrow = c1 >= b1 && c1 < e1 && c2 >= b2 && c2 < e2;
     if (!inrow) {
       for (int x = lane; x < L.P[0]; x += 32) out[base + x] = in[base + x];
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(256) lope_k_fill_hash(T* __restrict__ buf, Dev
     const unsigned long long z = lope_splitmix64(g + seed * 0x9E3779B97F4A7C15ULL);
     const double v = (double)(z >> 11) * (1.0 / 9007199254740992.0);
     const double u = 2.0 * v - 1.0;
-    buf[(i + L.lo[0]) + (j + L.lo[1]) * L.S1 + (k + L.lo[2]) * L.S2] = (T)u;
+    buf[L.B + (i + L.lo[0]) + (j + L.lo[1]) * L.S1 + (k + L.lo[2]) * L.S2] = (T)u;
   }
 }
 
@@ -252,7 +253,7 @@ template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
 template <class T> struct HScal { T v[16]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
-  int wrap, zchunk;
+  int wrap, zchunk, xshift, box0;
 };
 
 }  // namespace
@@ -295,35 +296,38 @@ void write_file_atomic(const std::string& p, const std::vector<char>& data) {
   std::rename(tmp.c_str(), p.c_str());
 }
 
+int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
+  int sz = dtype == LOPE_F32 ? 4 : 8;
+  int vec = 16 / sz;
+  int bx = 32 * c.bxw, by = c.wy * c.ry;
+  int boxx = ((k.fn[0][0] + bx + k.fp[0][0] + 2 * (vec - 1)) / vec) * vec;
+  int boxy = by + k.fn[0][1] + k.fp[0][1];
+  int stage = ((boxx * boxy * sz + 127) / 128) * 128;
+  if (boxx > 256 || boxy > 256) return 1 << 30;
+  return c.ns * stage + 2 * c.ns * 8;
+}
+
 TileCfg pick_tile(const lope::Kir& k, int dtype) {
+  // Calibrated on B200 (tools/tmabench.cu): 2 CTAs/SM, ~10 ring slots of a
+  // 128-column tile keep enough TMA bytes in flight to run near the copy roofline.
   TileCfg c;
-  if (dtype == LOPE_F32) {
-    if (k.rank == 3) { c.bxw = 4; c.wy = 2; c.ry = 8; }
-    else             { c.bxw = 4; c.wy = 4; c.ry = 8; }
-  } else {
-    if (k.rank == 3) { c.bxw = 2; c.wy = 2; c.ry = 8; }
-    else             { c.bxw = 2; c.wy = 4; c.ry = 8; }
-  }
   int nzw = k.fn[0][2] + k.fp[0][2] + 1;
-  c.ns = k.rank == 3 ? nzw + 5 : 4;
+  if (dtype == LOPE_F32) {
+    c.bxw = 4; c.wy = 2; c.ry = 8; c.ns = 10;
+  } else {
+    if (k.rank == 3) { c.bxw = 2; c.wy = 2; c.ry = 8; c.ns = 10; }
+    else             { c.bxw = 2; c.wy = 4; c.ry = 8; c.ns = 5; }
+  }
+  if (c.ns < nzw + 1) c.ns = nzw + 1;
   if (const char* e = std::getenv("LOPE_TILE")) {
     int a, b, cc, d;
     if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &cc, &d) == 4) {
       c.bxw = a; c.wy = b; c.ry = cc; c.ns = d < nzw + 1 ? nzw + 1 : d;
     }
   }
+  // shrink the ring until two CTAs fit on an SM (227 KB)
+  while (c.ns > nzw + 1 && 2 * tiled_smem_bytes(k, dtype, c) > 225 * 1024) --c.ns;
   return c;
-}
-
-int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
-  int sz = dtype == LOPE_F32 ? 4 : 8;
-  int vec = 16 / sz;
-  int bx = 32 * c.bxw, by = c.wy * c.ry;
-  int boxx = ((k.fn[0][0] + bx + k.fp[0][0] + vec - 1) / vec) * vec;
-  int boxy = by + k.fn[0][1] + k.fp[0][1];
-  int stage = ((boxx * boxy * sz + 127) / 128) * 128;
-  if (boxx > 256 || boxy > 256) return 1 << 30;
-  return c.ns * stage + c.ns * 8;
 }
 
 std::string build_source(lope_kernel* K) {
@@ -334,7 +338,7 @@ std::string build_source(lope_kernel* K) {
   const char* T = K->dtype == LOPE_F32 ? "float" : "double";
   s << "typedef " << T << " LT;\n";
   s << "struct LopeArrPack { LopeArr<LT> a[" << k.arrays.size() << "]; };\n";
-  s << "extern \"C\" __global__ void __launch_bounds__(256) lope_generic("
+  s << "extern \"C\" __global__ void __launch_bounds__(128) lope_generic("
        "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
        "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n}\n";
   if (K->tiled_ok) {
@@ -343,7 +347,7 @@ std::string build_source(lope_kernel* K) {
       << "> LopeCfg;\n";
     s << "extern \"C\" __constant__ int lope_tiled_info[4] = {LopeCfg::SMEM_BYTES, LopeCfg::THREADS, "
          "LopeCfg::BOXX, LopeCfg::BOXY};\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * c.bxw * c.wy
+    s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (c.bxw * c.wy + 1)
       << ", 2) lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
@@ -464,7 +468,7 @@ HScal<T> make_scal(const lope::Kir& k, const double* rs, const int64_t* is) {
 }
 
 int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtensorMap* map) {
-  cuuint64_t dims[3] = {(cuuint64_t)L->padded[0], (cuuint64_t)L->padded[1], (cuuint64_t)L->padded[2]};
+  cuuint64_t dims[3] = {(cuuint64_t)L->stride[1], (cuuint64_t)L->padded[1], (cuuint64_t)L->padded[2]};
   cuuint64_t strides[2] = {(cuuint64_t)(L->stride[1] * L->elem_bytes), (cuuint64_t)(L->stride[2] * L->elem_bytes)};
   cuuint32_t box[3] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy, 1};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -505,6 +509,12 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   }
   g.wrap = wrap;
   g.zchunk = zchunk_default(k);
+  {
+    const int vec = 16 / (int)sizeof(T);
+    const long long start = layouts[0].base + layouts[0].lo[0] + r0[0] - k.fn[0][0];
+    g.xshift = (int)(((start % vec) + vec) % vec);
+    g.box0 = (int)(start - g.xshift);
+  }
   Drv& d = drv();
   const bool use_tiled = K->tiled_ok && k.arrays.size() == 1 && !std::getenv("LOPE_FORCE_GENERIC");
   if (use_tiled) {
@@ -516,13 +526,14 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     a.out = (T*)out[0];
     a.s1 = L->stride[1];
     a.s2 = L->stride[2];
-    a.org = (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+    a.org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
             (long long)(L->lo[2] + r0[2]) * L->stride[2];
     const TileCfg& c = K->tile;
     long long ntx = (ext[0] + 32 * c.bxw - 1) / (32 * c.bxw);
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     long long units = ntx * nty * nzc;
+    if (units >= (1LL << 31)) return fail(108, "launch range too large for the tiled path");
     long long grid = (long long)m->tiled_blocks * sm_count();
     if (const char* e = std::getenv("LOPE_GRID")) grid = std::atoll(e);
     if (grid > units) grid = units;
@@ -541,16 +552,14 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     pack[i].out = out ? (T*)out[i] : nullptr;
     pack[i].s1 = L->stride[1];
     pack[i].s2 = L->stride[2];
-    pack[i].org = (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+    pack[i].org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
                   (long long)(L->lo[2] + r0[2]) * L->stride[2];
   }
-  long long n = (long long)ext[0] * ext[1] * ext[2];
-  long long grid = (n + 255) / 256;
-  long long cap = (long long)sm_count() * 8;
-  if (grid > cap) grid = cap;
-  if (grid < 1) grid = 1;
+  unsigned gx = (unsigned)((ext[0] + 127) / 128);
+  unsigned gy = (unsigned)(ext[1] < 65535 ? ext[1] : 65535);
+  unsigned gz = (unsigned)(ext[2] < 65535 ? ext[2] : 65535);
   void* args[] = {pack.data(), &sc, &g};
-  CUresult r = d.launchKernel(m->generic, (unsigned)grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr);
+  CUresult r = d.launchKernel(m->generic, gx, gy, gz, 128, 1, 1, 0, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_generic)");
   g_launches++;
   return 0;
@@ -635,9 +644,14 @@ int lope_layout_init(lope_layout* out, int32_t rank, int32_t dtype, const int64_
     }
     L.padded[d] = L.interior[d] + L.lo[d] + L.hi[d];
   }
-  const int64_t vec = 16 / L.elem_bytes;
+  const int64_t line = 128 / L.elem_bytes;             // elements per 128-byte line
+  const int64_t ox = ((L.lo[0] + line - 1) / line) * line;   // interior x origin, line aligned
+  L.base = ox - L.lo[0];
   L.stride[0] = 1;
-  L.stride[1] = ((L.padded[0] + vec - 1) / vec) * vec;
+  // at least one 32-byte sector of padding after the high halo (whole-sector halo stores)
+  const int64_t sec = 32 / L.elem_bytes;
+  const int64_t tail = L.hi[0] > sec ? L.hi[0] : sec;
+  L.stride[1] = ((ox + L.interior[0] + tail + line - 1) / line) * line;
   L.stride[2] = L.stride[1] * L.padded[1];
   L.count = L.stride[2] * L.padded[2];
   *out = L;
@@ -818,8 +832,8 @@ static int pack_impl(const lope_layout* L, const void* host, void* dev, cudaStre
   const size_t eb = (size_t)L->elem_bytes;
   cudaPitchedPtr hp = make_cudaPitchedPtr(const_cast<void*>(host), L->interior[0] * eb, L->interior[0],
                                           L->interior[1]);
-  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, L->stride[1] * eb, L->padded[0], L->padded[1]);
-  cudaPos dpos = make_cudaPos(L->lo[0] * eb, L->lo[1], L->lo[2]);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, L->stride[1] * eb, L->stride[1], L->padded[1]);
+  cudaPos dpos = make_cudaPos((L->base + L->lo[0]) * eb, L->lo[1], L->lo[2]);
   p.extent = make_cudaExtent(L->interior[0] * eb, L->interior[1], L->interior[2]);
   if (to_dev) {
     p.srcPtr = hp;
@@ -879,6 +893,7 @@ int lope_face_span(const lope_layout* L, int32_t which, int64_t* offset, int64_t
     case 3: *offset = m * plane; *count = lo * plane; break;               // last `lo` interior planes
     default: return fail(108, "face selector %d outside 0..3", which);
   }
+  if (d == 0) *offset += L->base;       // rank 1: "planes" are single elements of the row
   return 0;
 }
 

@@ -77,13 +77,15 @@ struct LopeGeom {
   int lo[3], hi[3];
   int wrap;       // bit d: refresh periodic halo images along dim d in the epilogue
   int zchunk;     // tiled: planes per work unit
+  int xshift;     // tiled: elements the TMA box starts early so its start is 16-byte aligned
+  int box0;       // tiled: TMA x coordinate of tile 0's box (row-relative, already shifted)
 };
 
 // --------------------------------------------------------------------------
 // Periodic-image epilogue
 
 template <class T>
-__device__ __forceinline__ void lope_store_images(T* __restrict__ out, lope_i64 s1, lope_i64 s2,
+__device__ __noinline__ void lope_store_images(T* __restrict__ out, lope_i64 s1, lope_i64 s2,
                                                   lope_i64 org0, int x, int y, int z,
                                                   const LopeGeom& g, T v) {
   // (x,y,z) are 0-based interior coordinates; org0 = flat offset of interior (0,0,0).
@@ -126,34 +128,40 @@ template <class T> struct LopeGlobalReader {
   }
 };
 
+__device__ __forceinline__ bool lope_near(int c, int m, int lo, int hi) {
+  return c < hi || c >= m - lo;
+}
+
+// Grid: x = blockIdx.x*blockDim.x + threadIdx.x, rows over blockIdx.y, planes over
+// blockIdx.z (grid-stride in each), so there is no per-point division.
 template <class Body, class T>
 __device__ __forceinline__ void lope_generic_impl(const LopeArr<T>* arrs, const LopeScal<T>& sc,
                                                   const LopeGeom& g) {
-  const lope_i64 nx = g.ext[0], ny = g.ext[1], nz = g.ext[2];
-  const lope_i64 n = nx * ny * nz;
-  for (lope_i64 t = (lope_i64)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (lope_i64)gridDim.x * blockDim.x) {
-    const int i = (int)(t % nx);
-    const lope_i64 r = t / nx;
-    const int j = (int)(r % ny);
-    const int k = (int)(r / ny);
-    LopeGlobalReader<T> rd;
-    rd.a = arrs;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.ext[0]) return;
+  const bool xn = (g.wrap & 1) && lope_near(i + g.r0[0], g.m[0], g.lo[0], g.hi[0]);
+  for (int k = blockIdx.z; k < g.ext[2]; k += gridDim.z) {
+    const bool zn = (g.wrap & 4) && lope_near(k + g.r0[2], g.m[2], g.lo[2], g.hi[2]);
+    for (int j = blockIdx.y; j < g.ext[1]; j += gridDim.y) {
+      const bool yn = (g.wrap & 2) && lope_near(j + g.r0[1], g.m[1], g.lo[1], g.hi[1]);
+      LopeGlobalReader<T> rd;
+      rd.a = arrs;
 #pragma unroll
-    for (int q = 0; q < Body::NARR; ++q)
-      rd.offs[q] = arrs[q].org + i + (lope_i64)j * arrs[q].s1 + (lope_i64)k * arrs[q].s2;
-    T res[Body::NSTORE > 0 ? Body::NSTORE : 1];
-    Body::template eval<T>(rd, sc.v, res);
+      for (int q = 0; q < Body::NARR; ++q)
+        rd.offs[q] = arrs[q].org + i + (lope_i64)j * arrs[q].s1 + (lope_i64)k * arrs[q].s2;
+      T res[Body::NSTORE > 0 ? Body::NSTORE : 1];
+      Body::template eval<T>(rd, sc.v, res);
 #pragma unroll
-    for (int q = 0; q < Body::NSTORE; ++q) {
-      const int A = Body::stored(q);
-      T* o = arrs[A].out;
-      o[rd.offs[A]] = res[q];
-      if (g.wrap) {
-        const lope_i64 org0 = arrs[A].org - g.r0[0] - (lope_i64)g.r0[1] * arrs[A].s1 -
-                              (lope_i64)g.r0[2] * arrs[A].s2;
-        lope_store_images<T>(o, arrs[A].s1, arrs[A].s2, org0, i + g.r0[0], j + g.r0[1],
-                             k + g.r0[2], g, res[q]);
+      for (int q = 0; q < Body::NSTORE; ++q) {
+        const int A = Body::stored(q);
+        T* o = arrs[A].out;
+        o[rd.offs[A]] = res[q];
+        if (xn | yn | zn) {
+          const lope_i64 org0 = arrs[A].org - g.r0[0] - (lope_i64)g.r0[1] * arrs[A].s1 -
+                                (lope_i64)g.r0[2] * arrs[A].s2;
+          lope_store_images<T>(o, arrs[A].s1, arrs[A].s2, org0, i + g.r0[0], j + g.r0[1],
+                               k + g.r0[2], g, res[q]);
+        }
       }
     }
   }
@@ -226,122 +234,185 @@ struct LopeTiledCfg {
   static constexpr int BX = 32 * BXW;
   static constexpr int BY = WY * RY;
   static constexpr int VEC = 16 / (int)sizeof(T);
-  static constexpr int BOXX = ((Body::FN0 + BX + Body::FP0 + VEC - 1) / VEC) * VEC;
+  // the box starts up to VEC-1 elements early (16-byte aligned TMA start), hence +VEC-1
+  static constexpr int BOXX = ((Body::FN0 + BX + Body::FP0 + VEC - 1 + VEC - 1) / VEC) * VEC;
   static constexpr int BOXY = BY + Body::FN1 + Body::FP1;
   static constexpr int NZW = Body::FN2 + Body::FP2 + 1;
   static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
   static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
-  static constexpr int SMEM_BYTES = NS * STAGE_BYTES + NS * 8;
-  static constexpr int THREADS = 32 * BXW * WY;
+  static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
+  static constexpr int NCW = BXW * WY;             // consumer (compute) warps
+  static constexpr int THREADS = 32 * (NCW + 1);   // + one TMA producer warp
 };
 
+__device__ __forceinline__ void lope_mbar_arrive(lope_u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lope_smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: warp NCW issues TMA loads into an NS-slot ring (full[s]:
+// TMA bytes landed; empty[s]: every compute warp is done with the slot); warps
+// 0..NCW-1 compute.  No CTA-wide barrier inside the loop, so warps drift within
+// the ring window and the producer runs up to NS loads ahead.
 template <class Body, class T, int BXW, int WY, int RY, int NS>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
   typedef LopeTiledCfg<Body, T, BXW, WY, RY, NS> C;
   static_assert(NS >= C::NZW + 1, "ring must hold the z window plus one prefetch slot");
   constexpr int FZN = Body::FN2;
+  constexpr int NZW = C::NZW;
   extern __shared__ __align__(128) unsigned char lope_smem[];
-  lope_u64* bars = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
+  lope_u64* full = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
+  lope_u64* empty = full + NS;
 
   const int ntx = (g.ext[0] + C::BX - 1) / C::BX;
   const int nty = (g.ext[1] + C::BY - 1) / C::BY;
   const int zc = g.zchunk;
   const int nzc = (g.ext[2] + zc - 1) / zc;
-  const lope_i64 nunits = (lope_i64)ntx * nty * nzc;
+  const int nunits = ntx * nty * nzc;     // < 2^31 (host checks)
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
     lope_tma_prefetch_desc(map);
-    for (int s = 0; s < NS; ++s) lope_mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      lope_mbar_init(&full[s], 1);
+      lope_mbar_init(&empty[s], C::NCW);
+    }
     lope_fence_init();
   }
   __syncthreads();
 
-  // producer cursor (thread 0 only)
-  lope_i64 p_unit = blockIdx.x;
-  int p_load = 0;
-  lope_i64 issued = 0;
-  // TMA box origin in padded coordinates for range-relative (0,0,0)
-  const int ox = g.lo[0] + g.r0[0] - Body::FN0;
-  const int oy = g.lo[1] + g.r0[1] - Body::FN1;
-  const int oz = g.lo[2] + g.r0[2];
+  if (warp == C::NCW) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const int ox = g.box0;
+      const int oy = g.lo[1] + g.r0[1] - Body::FN1;
+      const int oz = g.lo[2] + g.r0[2] - FZN;
+      lope_u32 L = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int tx = u % ntx;
+        const int r_ = u / ntx;
+        const int ty = r_ % nty;
+        const int z0 = (r_ / nty) * zc;
+        const int nl = min(zc, g.ext[2] - z0) + NZW - 1;
+        for (int pl = 0; pl < nl; ++pl, ++L) {
+          const lope_u32 slot = L % NS;
+          if (L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
+          lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
+          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], ox + tx * C::BX,
+                           oy + ty * C::BY, oz + z0 + pl);
+        }
+      }
+    }
+    return;
+  }
 
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  // ---------------- compute warps ----------------
   const int wx = warp % BXW;
   const int wy = warp / BXW;
   const int col = wx * 32 + lane;          // column within the tile
   const int row0 = wy * RY;                // first row within the tile
+  const lope_i64 s1 = a.s1, s2 = a.s2;
+  const lope_i64 org0 = a.org - g.r0[0] - (lope_i64)g.r0[1] * s1 - (lope_i64)g.r0[2] * s2;
 
-  lope_i64 lbase = 0;
-  for (lope_i64 u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int tx = (int)(u % ntx);
-    const lope_i64 r_ = u / ntx;
-    const int ty = (int)(r_ % nty);
-    const int zi = (int)(r_ / nty);
-    const int z0 = zi * zc;
+  lope_u32 lbase = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int tx = u % ntx;
+    const int r_ = u / ntx;
+    const int ty = r_ % nty;
+    const int z0 = (r_ / nty) * zc;
     const int nz = min(zc, g.ext[2] - z0);
     const int x = tx * C::BX + col;
+    const int ybase = ty * C::BY + row0;
     const bool xok = x < g.ext[0];
-    for (int pz = 0; pz < nz; ++pz) {
-      __syncthreads();   // every thread is done with the previous plane: its oldest slot is free
-      if (threadIdx.x == 0) {
-        const lope_i64 lowest = lbase + pz;
-        while (issued < lowest + NS && p_unit < nunits) {
-          const int ptx = (int)(p_unit % ntx);
-          const lope_i64 pr = p_unit / ntx;
-          const int pty = (int)(pr % nty);
-          const int pzi = (int)(pr / nty);
-          const int pz0 = pzi * zc;
-          const int pnz = min(zc, g.ext[2] - pz0);
-          const int slot = (int)(issued % NS);
-          lope_mbar_expect_tx(&bars[slot], C::TX_BYTES);
-          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &bars[slot], ox + ptx * C::BX,
-                           oy + pty * C::BY, oz + pz0 - FZN + p_load);
-          ++issued;
-          if (++p_load == pnz + C::NZW - 1) {
-            p_load = 0;
-            p_unit += gridDim.x;
-          }
-        }
-      }
-      LopeSmemReader<T, C::BOXX, C::NZW, FZN> rd;
+    // Periodic-image epilogue, precomputed per lane (x) / per warp row (y) / per plane
+    // (z): each dim has at most one image when m >= lo + hi; smaller interiors take
+    // the general (rare, slow) path.
+    // x images are written a whole 32-byte sector at a time: the SEC boundary lanes
+    // whose images land in the halo sector all store, padding cells included (the
+    // layout reserves a sector of padding on each side), so no partial-sector
+    // writes reach DRAM.
+    constexpr int SEC = 32 / (int)sizeof(T);
+    const int xg = x + g.r0[0];
+    const bool xw = (g.wrap & 1) && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
+    const int ximg = xg < SEC ? g.m[0] : -g.m[0];       // x image offset (if xw)
+    const bool one_x = g.m[0] >= 2 * SEC;
+    const bool one_y = g.m[1] >= g.lo[1] + g.hi[1];
+    const bool one_z = g.m[2] >= g.lo[2] + g.hi[2];
+    const bool simple = one_x && one_y && one_z;
+    T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
+    for (int pz = 0; pz < nz; ++pz, orow += s2) {
+      LopeSmemReader<T, C::BOXX, NZW, FZN> rd;
 #pragma unroll
-      for (int w = 0; w < C::NZW; ++w) {
-        const lope_i64 L = lbase + pz + w;
-        const int slot = (int)(L % NS);
-        lope_mbar_wait(&bars[slot], (lope_u32)((L / NS) & 1));
+      for (int w = 0; w < NZW; ++w) {
+        const lope_u32 L = lbase + pz + w;
+        const lope_u32 slot = L % NS;
+        lope_mbar_wait(&full[slot], (L / NS) & 1);
         rd.sp[w] = reinterpret_cast<const T*>(lope_smem + slot * C::STAGE_BYTES) +
-                   (row0 + Body::FN1) * C::BOXX + col + Body::FN0;
+                   (row0 + Body::FN1) * C::BOXX + col + Body::FN0 + g.xshift;
       }
-      const int z = z0 + pz;
-      const int ybase = ty * C::BY + row0;
       T vals[RY];
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
-        LopeSmemReader<T, C::BOXX, C::NZW, FZN> rr;
+        LopeSmemReader<T, C::BOXX, NZW, FZN> rr;
 #pragma unroll
-        for (int w = 0; w < C::NZW; ++w) rr.sp[w] = rd.sp[w] + r * C::BOXX;
+        for (int w = 0; w < NZW; ++w) rr.sp[w] = rd.sp[w] + r * C::BOXX;
         T res[1];
         Body::template eval<T>(rr, sc.v, res);
         vals[r] = res[0];
       }
-      if (xok) {
-        const lope_i64 zoff = a.org + x + (lope_i64)z * a.s2;
+      // every smem read of this plane is done: release the oldest slot (and, at the
+      // end of the unit, the trailing z-halo slots)
+      __syncwarp();
+      if (lane == 0) {
+        lope_mbar_arrive(&empty[(lbase + pz) % NS]);
+        if (pz == nz - 1)
+          for (int w = 1; w < NZW; ++w) lope_mbar_arrive(&empty[(lbase + pz + w) % NS]);
+      }
+      if (!xok) continue;
+      const int zg = z0 + pz + g.r0[2];
+      const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
+      const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] : -(lope_i64)g.m[2]) * s2;
+      if (!g.wrap) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+          if (ybase + r < g.ext[1]) orow[(lope_i64)r * s1] = vals[r];
+      } else if (simple) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
-          const int y = ybase + r;
-          if (y < g.ext[1]) {
-            a.out[zoff + (lope_i64)y * a.s1] = vals[r];
-            if (g.wrap) {
-              const lope_i64 org0 = a.org - g.r0[0] - (lope_i64)g.r0[1] * a.s1 - (lope_i64)g.r0[2] * a.s2;
-              lope_store_images<T>(a.out, a.s1, a.s2, org0, x + g.r0[0], y + g.r0[1], z + g.r0[2], g,
-                                   vals[r]);
+          if (ybase + r >= g.ext[1]) continue;
+          T* p = orow + (lope_i64)r * s1;
+          const T v = vals[r];
+          p[0] = v;
+          if (xw) p[ximg] = v;
+          const int yg = ybase + r + g.r0[1];
+          const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
+          if (yw | zw) {
+            const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] : -(lope_i64)g.m[1]) * s1;
+            if (yw) {
+              p[yimg] = v;
+              if (xw) p[yimg + ximg] = v;
+            }
+            if (zw) {
+              p[zimg] = v;
+              if (xw) p[zimg + ximg] = v;
+              if (yw) {
+                p[zimg + yimg] = v;
+                if (xw) p[zimg + yimg + ximg] = v;
+              }
             }
           }
         }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+          if (ybase + r < g.ext[1]) {
+            orow[(lope_i64)r * s1] = vals[r];
+            lope_store_images<T>(a.out, s1, s2, org0, xg, ybase + r + g.r0[1], zg, g, vals[r]);
+          }
       }
     }
-    lbase += nz + C::NZW - 1;
+    lbase += nz + NZW - 1;
   }
 }

@@ -106,7 +106,7 @@ class HaloArray:
         L = self.layout
         p = [int(L.padded[d]) for d in range(3)]
         v = self.data.view(p[2], p[1], int(L.stride[1]))
-        return v[:, :, :p[0]]
+        return v[:, :, int(L.base):int(L.base) + p[0]]
 
     def interior_view(self):
         L = self.layout

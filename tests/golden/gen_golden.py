@@ -250,8 +250,15 @@ def gen_random():
     nrng = np.random.default_rng(12)
     arrays = {}
     meta = []
-    for trial in range(60):
-        rank = 2 if trial < 40 else (3 if trial < 52 else 1)
+    trial = -1
+    attempt = 0
+    while len(meta) < 60:
+        attempt += 1
+        n = len(meta)
+        rank = 2 if n < 40 else (3 if n < 52 else 1)
+        trial = n
+        if attempt > 100000:
+            raise RuntimeError("random kernel generation did not converge")
         use_scalars = trial % 3 == 0
         scal_names = ["c", "q"] if use_scalars else []
         body = ""
@@ -275,6 +282,10 @@ def gen_random():
                 f"end subroutine k\n\nprogram main\nend program main\n")
         result = compile_text(text)
         kir = lower_kernel(result.kernels["k"])
+        # keep only kernels whose stored value depends on the field at >= 2 offsets
+        n_reads = sum(repr(st.expr).count("Read(") for st in kir.body)
+        if n_reads < 2 or all(o == 0 for fp in kir.footprints.values() for d in fp.dims for o in d):
+            continue
         shape = {1: (11,), 2: (9, 7), 3: (7, 6, 5)}[rank]
         field = nrng.uniform(-1, 1, shape)
         scal = {"c": np.float64(0.75), "q": np.int64(3)} if use_scalars else {}

@@ -32,14 +32,19 @@ def test_layout_matches_reference_storage_layout():
     # StorageLayout((8,4,3),(1,2,0),(1,0,1)): padded (10,6,4) (tests/test_layout.py:24-29)
     L = _lib.make_layout(3, "f32", (8, 4, 3), (1, 2, 0), (1, 0, 1))
     assert tuple(L.padded) == (10, 6, 4)
-    # row pitch rounded to 16 bytes for TMA; otherwise column-major like the reference
-    assert L.stride[0] == 1 and L.stride[1] == 12 and L.stride[2] == 12 * 6
-    assert L.count == 12 * 6 * 4
-    # frozen KAT (test_layout.py:14-21): 8x4 interior, halo 1, centre (1,1)+(1,0) -> coords (2,1)
+    # column-major like the reference, each row shifted so the interior starts on a
+    # 128-byte line and the pitch rounded to whole lines
+    assert L.base == 32 - 1 and (L.base + L.lo[0]) % 32 == 0
+    assert L.stride[0] == 1 and L.stride[1] == 64 and L.stride[2] == 64 * 6
+    assert L.count == 64 * 6 * 4
+    # frozen KAT (test_layout.py:14-21): 8x4 interior, halo 1, centre (1,1)+(1,0) -> padded (2,1);
+    # the reference's linear index 12 = 2 + 1*10 becomes base + 2 + 1*stride here
     L2 = _lib.make_layout(2, "f64", (8, 4), (1, 1), (1, 1))
-    assert L2.stride[1] == 10      # 10 doubles = 80 B, already a 16 B multiple
-    assert 2 + 1 * L2.stride[1] == 12
-    assert 9 + 5 * L2.stride[1] == 59
+    assert L2.stride[1] == 32 and L2.base == 15
+    ref_linear = lambda c0, c1: c0 + c1 * 10
+    dev_linear = lambda c0, c1: L2.base + c0 + c1 * L2.stride[1]
+    assert ref_linear(2, 1) == 12 and ref_linear(9, 5) == 59
+    assert dev_linear(2, 1) == 15 + 2 + 32 and dev_linear(9, 5) == 15 + 9 + 5 * 32
 
 
 def test_layout_rejects_bad_shapes():
@@ -90,3 +95,15 @@ def test_bad_ir_is_rejected():
     assert e.value.code == "E104"
     with pytest.raises(RuntimeFault):
         _lib.compile_kernel("LOPE1\nkernel k 2\narray u\nstore u r u 0 0\nstore u r u 1 0\nend\n", "f32")
+
+
+def test_compiled_kernel_object_without_gpu():
+    from paper_1502_03504_b200.runtime import CompiledKernel
+    for dt in ("float32", "float64", _lib.F32):
+        k = CompiledKernel(stencils.drift2(), dt)
+        d = json.loads(k.describe())
+        assert d["scalars"] == [["c", "real"]] and d["footprints"] == [[[2, 0], [1, 1]]]
+        rs, is_ = k.scalar_args({"c": 0.25})
+        assert rs[0] == 0.25
+    with pytest.raises(RuntimeFault):
+        k.scalar_args({})

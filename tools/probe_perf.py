@@ -1,0 +1,45 @@
+"""Debug: time lope_step on the c3 workload under different tile/zchunk/grid settings."""
+import os, sys, pathlib, subprocess, json
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+import torch
+from paper_1502_03504_b200 import runtime as R, stencils
+shape = tuple(int(x) for x in os.environ.get("SHAPE", "1024,1024,1024").split(","))
+name = os.environ.get("KERNEL", "lap3d7")
+dt = os.environ.get("DT", "float32")
+if name == "copy3d":
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder("copy3d", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0]); kir = kb.build()
+elif name == "copy3dh":
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder("copy3dh", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0] + 0 * (u[1, 1, 0] + u[-1, -1, 0])); kir = kb.build()
+elif name == "copy3dz":
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder("copy3dz", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0] + 0 * (u[0, 0, 1] + u[0, 0, -1])); kir = kb.build()
+else:
+    kir = stencils.by_name(name)
+k = R.CompiledKernel(kir, dt)
+fp = kir.footprints[kir.array_params[0]].dims
+a = R.HaloArray(shape, [n for n, _ in fp], [p for _, p in fp], dt)
+a.fill_hash(1)
+R.halo_transfer(a)
+for _ in range(3):
+    R.step(k, a)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n = int(os.environ.get("N", "10"))
+e0.record()
+mode = os.environ.get("MODE", "step")
+for _ in range(n):
+    if mode == "step":
+        R.step(k, a)
+    else:
+        R.step(k, a, wrap_mask=0)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / n
+import numpy as np
+pts = np.prod(shape)
+esz = 4 if dt == "float32" else 8
+print(json.dumps({"env": {k_: os.environ.get(k_) for k_ in ("LOPE_TILE", "LOPE_ZCHUNK", "LOPE_GRID", "LOPE_FORCE_GENERIC")},
+                  "desc": json.loads(k.describe())["tile"], "ms": round(ms, 4), "gpts": round(pts / ms / 1e6, 1),
+                  "GBs": round(2 * esz * pts / ms / 1e6, 1)}), flush=True)
