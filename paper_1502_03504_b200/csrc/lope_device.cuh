@@ -291,10 +291,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       const int oz = g.lo[2] + g.r0[2] - FZN;
       lope_u32 L = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int tx = u % ntx;
-        const int r_ = u / ntx;
-        const int ty = r_ % nty;
-        const int z0 = (r_ / nty) * zc;
+        const int ty = u % nty;            // y fastest: neighbours in y run concurrently and
+        const int r_ = u / nty;            // x-edge tiles rotate over CTAs
+        const int tx = r_ % ntx;
+        const int z0 = (r_ / ntx) * zc;
         const int nl = min(zc, g.ext[2] - z0) + NZW - 1;
         for (int pl = 0; pl < nl; ++pl, ++L) {
           const lope_u32 slot = L % NS;
@@ -318,10 +318,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
 
   lope_u32 lbase = 0;
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int tx = u % ntx;
-    const int r_ = u / ntx;
-    const int ty = r_ % nty;
-    const int z0 = (r_ / nty) * zc;
+    const int ty = u % nty;
+    const int r_ = u / nty;
+    const int tx = r_ % ntx;
+    const int z0 = (r_ / ntx) * zc;
     const int nz = min(zc, g.ext[2] - z0);
     const int x = tx * C::BX + col;
     const int ybase = ty * C::BY + row0;
@@ -329,11 +329,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
     // Periodic-image epilogue, precomputed per lane (x) / per warp row (y) / per plane
     // (z): each dim has at most one image when m >= lo + hi; smaller interiors take
     // the general (rare, slow) path.
-    // x images are written a whole 32-byte sector at a time: the SEC boundary lanes
-    // whose images land in the halo sector all store, padding cells included (the
-    // layout reserves a sector of padding on each side), so no partial-sector
-    // writes reach DRAM.
-    constexpr int SEC = 32 / (int)sizeof(T);
+    // x images are written a whole 64-byte atom at a time: the SEC boundary lanes
+    // whose images land in the halo atom all store, padding cells included (the
+    // layout reserves an atom on each side), so no partial atoms reach DRAM.
+    constexpr int SEC = 64 / (int)sizeof(T);          // one 64-byte DRAM atom
     const int xg = x + g.r0[0];
     const bool xw = (g.wrap & 1) && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
     const int ximg = xg < SEC ? g.m[0] : -g.m[0];       // x image offset (if xw)
@@ -341,6 +340,12 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
     const bool one_y = g.m[1] >= g.lo[1] + g.hi[1];
     const bool one_z = g.m[2] >= g.lo[2] + g.hi[2];
     const bool simple = one_x && one_y && one_z;
+    // warp-uniform: does any lane of this warp have an x image, or any of its rows a y image?
+    const bool wx_any = __any_sync(0xffffffffu, xw && xok);
+    const bool wy_any = (g.wrap & 2) && (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                                         lope_near(min(ybase + RY - 1, g.ext[1] - 1) + g.r0[1], g.m[1],
+                                                   g.lo[1], g.hi[1]) ||
+                                         !one_y);
     T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
     for (int pz = 0; pz < nz; ++pz, orow += s2) {
       LopeSmemReader<T, C::BOXX, NZW, FZN> rd;
@@ -374,10 +379,25 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       const int zg = z0 + pz + g.r0[2];
       const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
       const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] : -(lope_i64)g.m[2]) * s2;
-      if (!g.wrap) {
+      if (!(wy_any | zw) && simple) {
+        // no y/z images in this warp-plane: plain stores, plus the x-image sector store
+        // for the few boundary lanes
+        if (!wx_any) {
 #pragma unroll
-        for (int r = 0; r < RY; ++r)
-          if (ybase + r < g.ext[1]) orow[(lope_i64)r * s1] = vals[r];
+          for (int r = 0; r < RY; ++r)
+            if (ybase + r < g.ext[1]) orow[(lope_i64)r * s1] = vals[r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < RY; ++r)
+            if (ybase + r < g.ext[1]) {
+              orow[(lope_i64)r * s1] = vals[r];
+#ifdef LOPE_XSAME
+              if (xw) orow[(lope_i64)r * s1] = vals[r];
+#else
+              if (xw) orow[(lope_i64)r * s1 + ximg] = vals[r];
+#endif
+            }
+        }
       } else if (simple) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {

@@ -33,18 +33,18 @@ def test_layout_matches_reference_storage_layout():
     L = _lib.make_layout(3, "f32", (8, 4, 3), (1, 2, 0), (1, 0, 1))
     assert tuple(L.padded) == (10, 6, 4)
     # column-major like the reference, each row shifted so the interior starts on a
-    # 128-byte line and the pitch rounded to whole lines
-    assert L.base == 32 - 1 and (L.base + L.lo[0]) % 32 == 0
-    assert L.stride[0] == 1 and L.stride[1] == 64 and L.stride[2] == 64 * 6
-    assert L.count == 64 * 6 * 4
+    # 64-byte atom with an atom of room for each halo side, pitch in whole atoms
+    assert L.base == 16 - 1 and (L.base + L.lo[0]) % 16 == 0
+    assert L.stride[0] == 1 and L.stride[1] == 48 and L.stride[2] == 48 * 6
+    assert L.count == 48 * 6 * 4
     # frozen KAT (test_layout.py:14-21): 8x4 interior, halo 1, centre (1,1)+(1,0) -> padded (2,1);
     # the reference's linear index 12 = 2 + 1*10 becomes base + 2 + 1*stride here
     L2 = _lib.make_layout(2, "f64", (8, 4), (1, 1), (1, 1))
-    assert L2.stride[1] == 32 and L2.base == 15
+    assert L2.stride[1] == 24 and L2.base == 7
     ref_linear = lambda c0, c1: c0 + c1 * 10
     dev_linear = lambda c0, c1: L2.base + c0 + c1 * L2.stride[1]
     assert ref_linear(2, 1) == 12 and ref_linear(9, 5) == 59
-    assert dev_linear(2, 1) == 15 + 2 + 32 and dev_linear(9, 5) == 15 + 9 + 5 * 32
+    assert dev_linear(2, 1) == 7 + 2 + 24 and dev_linear(9, 5) == 7 + 9 + 5 * 24
 
 
 def test_layout_rejects_bad_shapes():

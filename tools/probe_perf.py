@@ -32,6 +32,8 @@ mode = os.environ.get("MODE", "step")
 for _ in range(n):
     if mode == "step":
         R.step(k, a)
+    elif mode.startswith("mask"):
+        R.step(k, a, wrap_mask=int(mode[4:]))
     else:
         R.step(k, a, wrap_mask=0)
 e1.record()
