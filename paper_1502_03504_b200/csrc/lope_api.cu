@@ -239,6 +239,7 @@ namespace {
 
 struct TileCfg {
   int bxw = 4, wy = 2, ry = 8, ns = 8;
+  int mb = 2;     // CTAs per SM the launch bounds target
 };
 
 struct DevMod {
@@ -253,7 +254,7 @@ template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
 template <class T> struct HScal { T v[16]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
-  int wrap, zchunk, xshift, box0;
+  int wrap, zchunk, xshift, box0, p1;
 };
 
 }  // namespace
@@ -297,10 +298,12 @@ void write_file_atomic(const std::string& p, const std::vector<char>& data) {
 }
 
 int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
+  // mirrors LopeTiledCfg (lope_device.cuh)
   int sz = dtype == LOPE_F32 ? 4 : 8;
-  int vec = 16 / sz;
-  int bx = 32 * c.bxw, by = c.wy * c.ry;
-  int boxx = ((k.fn[0][0] + bx + k.fp[0][0] + 2 * (vec - 1)) / vec) * vec;
+  int vx = 16 / sz;
+  int bx = 32 * vx * c.bxw, by = c.wy * c.ry;
+  int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
+  int boxx = padx + bx + ((k.fp[0][0] + vx - 1) / vx) * vx;
   int boxy = by + k.fn[0][1] + k.fp[0][1];
   int stage = ((boxx * boxy * sz + 127) / 128) * 128;
   if (boxx > 256 || boxy > 256) return 1 << 30;
@@ -308,25 +311,45 @@ int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
 }
 
 TileCfg pick_tile(const lope::Kir& k, int dtype) {
-  // Calibrated on B200 (tools/tmabench.cu): 2 CTAs/SM, ~10 ring slots of a
-  // 128-column tile keep enough TMA bytes in flight to run near the copy roofline.
+  // Lanes hold 16-byte vectors (4 fp32 / 2 fp64); tiles are one warp (128 fp32 /
+  // 64 fp64 columns) wide so the TMA box stays within 256 elements, with 8 compute
+  // warps stacked in y.  The ring is as deep as two CTAs per SM allow (calibrated
+  // with tools/tmabench.cu: ~10 slots of a ~10 KB box keep the copy roofline).
   TileCfg c;
-  int nzw = k.fn[0][2] + k.fp[0][2] + 1;
-  if (dtype == LOPE_F32) {
-    c.bxw = 4; c.wy = 2; c.ry = 8; c.ns = 10;
-  } else {
-    if (k.rank == 3) { c.bxw = 2; c.wy = 2; c.ry = 8; c.ns = 10; }
-    else             { c.bxw = 2; c.wy = 4; c.ry = 8; c.ns = 5; }
+  const int nzw = k.fn[0][2] + k.fp[0][2] + 1;
+  bool zstar = k.rank == 3;
+  for (const lope::Node& n : k.nodes)
+    if (n.kind == lope::Node::READ && n.arr == 0 && n.off[2] != 0 && (n.off[0] != 0 || n.off[1] != 0)) zstar = false;
+  const int hold = (zstar && k.fn[0][2] > 0) ? k.fp[0][2] + 1 : nzw;
+  c.bxw = 1;
+  c.wy = 8;
+  c.ry = k.rank == 3 ? 2 : 4;
+  c.ns = 16;
+  // Keep the per-lane register window (rows x columns of the centre plane, in 32-bit
+  // registers) small enough that nothing spills: at 2 CTAs/SM ptxas caps the kernel at
+  // 96 registers; wide footprints get one CTA per SM (up to ~128 registers) instead.
+  // Spills are not just slow here: local-memory traffic goes through L2 and evicts the
+  // halo lines neighbouring tiles would otherwise reuse.
+  {
+    const int vx = dtype == LOPE_F32 ? 4 : 2;
+    const int words = dtype == LOPE_F32 ? 1 : 2;
+    auto window = [&](int ry) {
+      return (ry + k.fn[0][1] + k.fp[0][1]) * (vx + k.fn[0][0] + k.fp[0][0]) * words;
+    };
+    while (c.ry > 2 && window(c.ry) > 40) c.ry /= 2;
+    if (window(c.ry) > 40) c.mb = 1;
   }
-  if (c.ns < nzw + 1) c.ns = nzw + 1;
   if (const char* e = std::getenv("LOPE_TILE")) {
     int a, b, cc, d;
     if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &cc, &d) == 4) {
-      c.bxw = a; c.wy = b; c.ry = cc; c.ns = d < nzw + 1 ? nzw + 1 : d;
+      c.bxw = a; c.wy = b; c.ry = cc; c.ns = d;
     }
   }
-  // shrink the ring until two CTAs fit on an SM (227 KB)
-  while (c.ns > nzw + 1 && 2 * tiled_smem_bytes(k, dtype, c) > 225 * 1024) --c.ns;
+  if (const char* e = std::getenv("LOPE_MB")) c.mb = std::atoi(e) == 1 ? 1 : 2;
+  if (c.mb == 1 && !std::getenv("LOPE_TILE")) c.ns = 32;
+  if (c.ns < hold + 1) c.ns = hold + 1;
+  // shrink the ring until mb CTAs fit on an SM (227 KB)
+  while (c.ns > hold + 1 && c.mb * tiled_smem_bytes(k, dtype, c) > 225 * 1024) --c.ns;
   return c;
 }
 
@@ -348,7 +371,7 @@ std::string build_source(lope_kernel* K) {
     s << "extern \"C\" __constant__ int lope_tiled_info[4] = {LopeCfg::SMEM_BYTES, LopeCfg::THREADS, "
          "LopeCfg::BOXX, LopeCfg::BOXY};\n";
     s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (c.bxw * c.wy + 1)
-      << ", 2) lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
+      << ", " << c.mb << ") lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
       << ">(&map, a, sc, g);\n}\n";
@@ -474,7 +497,43 @@ HScal<T> make_scal(const lope::Kir& k, const double* rs, const int64_t* is) {
   return s;
 }
 
+CUtensorMapL2promotion l2promo() {
+  static int v = -1;
+  if (v < 0) {
+    v = 2;   // 128-byte promotion: measured ~5% fewer HBM bytes than 256 B for the stencil boxes
+    if (const char* e = std::getenv("LOPE_L2PROMO")) v = std::atoi(e) & 3;
+  }
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
+bool tmap_flat() {
+  static int v = -1;
+  if (v < 0) {
+    v = 0;
+    if (const char* e = std::getenv("LOPE_TMAP2D")) v = std::atoi(e) != 0;
+  }
+  return v;
+}
+
 int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtensorMap* map) {
+  if (tmap_flat()) {
+    // planes stacked as rows: one 2-D map over padded1*padded2 rows
+    cuuint64_t dims2[2] = {(cuuint64_t)L->stride[1], (cuuint64_t)(L->padded[1] * L->padded[2])};
+    cuuint64_t strides2[1] = {(cuuint64_t)(L->stride[1] * L->elem_bytes)};
+    cuuint32_t box2[2] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy};
+    cuuint32_t estr2[2] = {1, 1};
+    CUresult r2 = drv().tensorMapEncodeTiled(
+        map, L->dtype == LOPE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+        const_cast<void*>(base), dims2, strides2, box2, estr2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, l2promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r2 != CUDA_SUCCESS) return cu_fail(r2, "cuTensorMapEncodeTiled(2d)");
+    return 0;
+  }
   cuuint64_t dims[3] = {(cuuint64_t)L->stride[1], (cuuint64_t)L->padded[1], (cuuint64_t)L->padded[2]};
   cuuint64_t strides[2] = {(cuuint64_t)(L->stride[1] * L->elem_bytes), (cuuint64_t)(L->stride[2] * L->elem_bytes)};
   cuuint32_t box[3] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy, 1};
@@ -482,7 +541,7 @@ int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtenso
   CUresult r = drv().tensorMapEncodeTiled(
       map, L->dtype == LOPE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
       const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CU_TENSOR_MAP_SWIZZLE_NONE, l2promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
   return 0;
 }
@@ -493,7 +552,7 @@ int zchunk_default(const lope::Kir& k) {
     int v = std::atoi(e);
     if (v > 0) return v;
   }
-  return 16;
+  return 64;   // z-halo planes re-read once per 64 planes (3%), balance within ~4%
 }
 
 // Launch the body kernel over `ranges` (0-based start r0, extents ext) of array set.
@@ -516,14 +575,27 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   }
   g.wrap = wrap;
   g.zchunk = zchunk_default(k);
+  const int vx = 16 / (int)sizeof(T);
   {
-    const int vec = 16 / (int)sizeof(T);
-    const long long start = layouts[0].base + layouts[0].lo[0] + r0[0] - k.fn[0][0];
-    g.xshift = (int)(((start % vec) + vec) % vec);
-    g.box0 = (int)(start - g.xshift);
+    const int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
+    g.xshift = 0;
+    g.box0 = (int)(layouts[0].base + layouts[0].lo[0] + r0[0] - padx);
+    g.p1 = tmap_flat() ? (int)layouts[0].padded[1] : 0;
   }
   Drv& d = drv();
-  const bool use_tiled = K->tiled_ok && k.arrays.size() == 1 && !std::getenv("LOPE_FORCE_GENERIC");
+  // the vector path needs 16-byte aligned x extents; when it refreshes halo images
+  // every halo cell must have exactly one image (interior at least two lines wide in
+  // x, at least lo+hi in y and z); other geometries run on the generic kernel
+  bool geom_ok = (r0[0] % vx) == 0 && (ext[0] % vx) == 0;
+  if (wrap) {
+    const lope_layout& L0 = layouts[0];
+    const long long line = 64 / (long long)sizeof(T);
+    geom_ok = geom_ok && L0.interior[0] % vx == 0 && L0.interior[0] >= 2 * line;
+    for (int d = 1; d < 3; ++d)
+      if ((wrap >> d) & 1) geom_ok = geom_ok && L0.interior[d] >= L0.lo[d] + L0.hi[d];
+  }
+  const bool use_tiled = K->tiled_ok && k.arrays.size() == 1 && geom_ok &&
+                         !std::getenv("LOPE_FORCE_GENERIC");
   if (use_tiled) {
     const lope_layout* L = &layouts[0];
     CUtensorMap map;
@@ -536,12 +608,16 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     a.org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
             (long long)(L->lo[2] + r0[2]) * L->stride[2];
     const TileCfg& c = K->tile;
-    long long ntx = (ext[0] + 32 * c.bxw - 1) / (32 * c.bxw);
+    long long ntx = (ext[0] + 32 * vx * c.bxw - 1) / (32 * vx * c.bxw);
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     long long units = ntx * nty * nzc;
     if (units >= (1LL << 31)) return fail(108, "launch range too large for the tiled path");
     long long grid = (long long)m->tiled_blocks * sm_count();
+    // units are walked x-fastest with stride `grid`: keep grid % ntx != 0 so the
+    // x-edge tiles (halo-image stores) rotate over the CTAs instead of piling up
+    if (ntx > 1)
+      while (grid > 1 && grid % ntx == 0) --grid;
     if (const char* e = std::getenv("LOPE_GRID")) grid = std::atoll(e);
     if (grid > units) grid = units;
     if (grid < 1) grid = 1;
@@ -679,7 +755,7 @@ int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kerne
   K->dtype = dtype;
   K->tile = pick_tile(K->ir, dtype);
   K->tiled_ok = K->ir.rank >= 2 && K->ir.arrays.size() == 1 &&
-                tiled_smem_bytes(K->ir, dtype, K->tile) <= 200 * 1024;
+                tiled_smem_bytes(K->ir, dtype, K->tile) <= 225 * 1024;
   K->source = build_source(K.get());
   std::string nm = "lope_" + K->ir.name;
   if (int e = nvrtc_compile(K->source, nm, &K->cubin)) return e;

@@ -265,7 +265,18 @@ struct Emitter {
       }
       case Node::ADD: return "A_::add(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
       case Node::MUL: return "A_::mul(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
-      case Node::DIV: return "A_::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      case Node::DIV: {
+        // x / 2^k == x * 2^-k exactly in IEEE arithmetic (same real value, one rounding),
+        // so a power-of-two constant divisor becomes a multiply (float and double alike)
+        const Node& d = k.nodes[n.kids[1]];
+        if (d.kind == Node::CONST && d.value != 0.0 && std::isfinite(d.value)) {
+          int e = 0;
+          double fr = std::frexp(d.value, &e);
+          if ((fr == 0.5 || fr == -0.5) && e > -100 && e < 100)
+            return "A_::mul(" + ex(n.kids[0]) + ", T(" + hexlit(1.0 / d.value) + "))";
+        }
+        return "A_::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      }
       case Node::NEG: return "A_::neg(" + ex(n.kids[0]) + ")";
       case Node::ABS: return "A_::abs_(" + ex(n.kids[0]) + ")";
       case Node::SQRT: return "A_::sqrt_(" + ex(n.kids[0]) + ")";
@@ -296,6 +307,12 @@ std::string emit_body(const Kir& k) {
     o << "  static constexpr int FN" << dn[d] << " = " << k.fn[0][d] << ";\n";
     o << "  static constexpr int FP" << dn[d] << " = " << k.fp[0][d] << ";\n";
   }
+  // ZSTAR: every read of array 0 off the centre plane is at x = y = 0 (past planes can
+  // live in registers in the tiled kernel)
+  bool zstar = k.rank == 3;
+  for (const Node& n : k.nodes)
+    if (n.kind == Node::READ && n.arr == 0 && n.off[2] != 0 && (n.off[0] != 0 || n.off[1] != 0)) zstar = false;
+  o << "  static constexpr bool ZSTAR = " << (zstar ? "true" : "false") << ";\n";
   o << "  static __device__ __forceinline__ constexpr int stored(int q) { return ";
   for (size_t i = 0; i + 1 < k.stored.size(); ++i) o << "q == " << i << " ? " << k.stored[i] << " : ";
   o << k.stored.back() << "; }\n";

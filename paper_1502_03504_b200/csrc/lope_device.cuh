@@ -79,6 +79,7 @@ struct LopeGeom {
   int zchunk;     // tiled: planes per work unit
   int xshift;     // tiled: elements the TMA box starts early so its start is 16-byte aligned
   int box0;       // tiled: TMA x coordinate of tile 0's box (row-relative, already shifted)
+  int p1;         // tiled: padded rows per plane; > 0 selects the flattened 2-D tensor map
 };
 
 // --------------------------------------------------------------------------
@@ -213,53 +214,131 @@ __device__ __forceinline__ void lope_tma_load_3d(void* dst, const LopeTmap* map,
       "l"((lope_u64)map), "r"(c0), "r"(c1), "r"(c2), "r"(lope_smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void lope_tma_load_2d(void* dst, const LopeTmap* map, lope_u64* bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(lope_smem_u32(dst)),
+      "l"((lope_u64)map), "r"(c0), "r"(c1), "r"(lope_smem_u32(bar))
+      : "memory");
+}
+#ifdef LOPE_TMA_EVICT_LAST
+__device__ __forceinline__ void lope_tma_load_2d_hint(void* dst, const LopeTmap* map, lope_u64* bar, int c0,
+                                                      int c1) {
+  lope_u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(lope_smem_u32(dst)),
+      "l"((lope_u64)map), "r"(c0), "r"(c1), "r"(lope_smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+#endif
 __device__ __forceinline__ void lope_tma_prefetch_desc(const LopeTmap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"((lope_u64)map) : "memory");
 }
 
 // --------------------------------------------------------------------------
-// Tiled TMA path
+// Tiled TMA path (vector lanes)
+//
+// Each lane owns VX = 16/sizeof(T) consecutive x points (one 16-byte vector) and
+// RY rows.  Per plane it loads the rows it needs from the staged box with 16-byte
+// LDS plus scalar LDS for the x halo into a register window (entries the body
+// never reads are dead code), evaluates the body VX*RY times from registers and
+// writes 16-byte vectors straight to HBM.  Stencils that are a star in z (every
+// read off the centre plane is at x = y = 0) keep the past planes in registers
+// (ZHIST), so a plane iteration holds only the centre and future planes of the ring.
 
-template <class T, int BOXX, int NZW, int FZN>
-struct LopeSmemReader {
-  const T* sp[NZW];   // per z offset: this thread's (column, first row) in that plane's box
+template <class T> struct LopeVec;
+template <> struct LopeVec<float> { typedef float4 V; };
+template <> struct LopeVec<double> { typedef double2 V; };
+
+#ifdef LOPE_ST_EVICT_FIRST
+__device__ __forceinline__ void lope_st_evict_first(float* p, float4 v) {
+  lope_u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void lope_st_evict_first(double* p, double2 v) {
+  lope_u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+#endif
+
+template <class T, int NR, int NXW, int FZN, int FN0, int FN1, int RY, int VX, bool ZHIST>
+struct LopeWinReader {
+  const T* win;    // [NZW][NR][NXW] register window (flattened)
+  const T* hist;   // [FZN][RY][VX] past planes at own points (ZHIST)
+  int r, v;        // compile-time after unrolling
   template <int A, int DX, int DY, int DZ>
   __device__ __forceinline__ T at() const {
-    return sp[DZ + FZN][DY * BOXX + DX];
+    if (ZHIST && DZ < 0) return hist[((-DZ - 1) * RY + r) * VX + v];
+    return win[((DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0)];
   }
 };
 
-template <class Body, class T, int BXW, int WY, int RY, int NS>
+template <class Body, class T, int WX, int WY, int RY, int NS>
 struct LopeTiledCfg {
-  static constexpr int BX = 32 * BXW;
+  static constexpr int VX = 16 / (int)sizeof(T);
+  static constexpr int BX = 32 * VX * WX;
   static constexpr int BY = WY * RY;
-  static constexpr int VEC = 16 / (int)sizeof(T);
-  // the box starts up to VEC-1 elements early (16-byte aligned TMA start), hence +VEC-1
-  static constexpr int BOXX = ((Body::FN0 + BX + Body::FP0 + VEC - 1 + VEC - 1) / VEC) * VEC;
+  static constexpr int PADX = ((Body::FN0 + VX - 1) / VX) * VX;
+  static constexpr int BOXX = PADX + BX + ((Body::FP0 + VX - 1) / VX) * VX;
   static constexpr int BOXY = BY + Body::FN1 + Body::FP1;
   static constexpr int NZW = Body::FN2 + Body::FP2 + 1;
+  static constexpr bool ZHIST = Body::ZSTAR && Body::FN2 > 0;
+  static constexpr int HOLD = ZHIST ? Body::FP2 + 1 : NZW;     // slots one plane iteration holds
   static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
   static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
   static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
-  static constexpr int NCW = BXW * WY;             // consumer (compute) warps
+  static constexpr int NCW = WX * WY;              // consumer (compute) warps
   static constexpr int THREADS = 32 * (NCW + 1);   // + one TMA producer warp
+  static constexpr int NR = RY + Body::FN1 + Body::FP1;
+  static constexpr int NXW = VX + Body::FN0 + Body::FP0;
 };
 
 __device__ __forceinline__ void lope_mbar_arrive(lope_u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lope_smem_u32(bar)) : "memory");
 }
 
-// Warp-specialised: warp NCW issues TMA loads into an NS-slot ring (full[s]:
-// TMA bytes landed; empty[s]: every compute warp is done with the slot); warps
-// 0..NCW-1 compute.  No CTA-wide barrier inside the loop, so warps drift within
-// the ring window and the producer runs up to NS loads ahead.
-template <class Body, class T, int BXW, int WY, int RY, int NS>
+// Division-free walk of the units u = b, b+G, b+2G, ... decomposed as
+// u = tx + ntx*(ty + nty*zi).  x is fastest: the CTAs of one round read x- and
+// y-neighbouring tiles at the same time, so the 128-byte lines tiles share at
+// their edges (and the halo rows) are fetched from HBM once and hit in L2 for the
+// neighbour.  The host picks G with G % ntx != 0 so x-edge tiles rotate over CTAs.
+struct LopeUnitWalk {
+  int tx, ty, zi, gtx, gty, gzi, ntx, nty;
+  __device__ __forceinline__ void init(int b, int G, int nty_, int ntx_) {
+    nty = nty_; ntx = ntx_;
+    tx = b % ntx; int r = b / ntx; ty = r % nty; zi = r / nty;
+    gtx = G % ntx; r = G / ntx; gty = r % nty; gzi = r / nty;
+  }
+  __device__ __forceinline__ void next() {
+    tx += gtx;
+    int c = 0;
+    if (tx >= ntx) { tx -= ntx; c = 1; }
+    ty += gty + c;
+    c = 0;
+    if (ty >= nty) { ty -= nty; c = 1; }
+    zi += gzi + c;
+  }
+};
+
+template <class Body, class T, int WX, int WY, int RY, int NS>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
-  typedef LopeTiledCfg<Body, T, BXW, WY, RY, NS> C;
-  static_assert(NS >= C::NZW + 1, "ring must hold the z window plus one prefetch slot");
-  constexpr int FZN = Body::FN2;
-  constexpr int NZW = C::NZW;
+  typedef LopeTiledCfg<Body, T, WX, WY, RY, NS> C;
+  typedef typename LopeVec<T>::V V;
+  constexpr int VX = C::VX;
+  constexpr int FZN = Body::FN2, FZP = Body::FP2;
+  constexpr int NZW = C::NZW, NR = C::NR, NXW = C::NXW;
+  constexpr bool ZHIST = C::ZHIST;
+  static_assert(NS >= C::HOLD + 1, "ring must hold the planes in use plus one prefetch slot");
+  static_assert(C::BOXX <= 256 && C::BOXY <= 256, "TMA box dimensions are limited to 256");
   extern __shared__ __align__(128) unsigned char lope_smem[];
   lope_u64* full = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
   lope_u64* empty = full + NS;
@@ -286,22 +365,37 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   if (warp == C::NCW) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const int ox = g.box0;
       const int oy = g.lo[1] + g.r0[1] - Body::FN1;
       const int oz = g.lo[2] + g.r0[2] - FZN;
+      LopeUnitWalk w;
+      w.init(blockIdx.x, gridDim.x, nty, ntx);
+#ifdef LOPE_STAGGER
+      // experiment: checkerboard start delay so neighbouring tiles do not miss in L2 together
+      if ((w.tx + w.ty) & 1) {
+        lope_u64 t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < (lope_u64)(LOPE_STAGGER));
+      }
+#endif
       lope_u32 L = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int ty = u % nty;            // y fastest: neighbours in y run concurrently and
-        const int r_ = u / nty;            // x-edge tiles rotate over CTAs
-        const int tx = r_ % ntx;
-        const int z0 = (r_ / ntx) * zc;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
+        const int z0 = w.zi * zc;
         const int nl = min(zc, g.ext[2] - z0) + NZW - 1;
+        const int bx = g.box0 + w.tx * C::BX, by = oy + w.ty * C::BY;
         for (int pl = 0; pl < nl; ++pl, ++L) {
           const lope_u32 slot = L % NS;
           if (L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
           lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
-          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], ox + tx * C::BX,
-                           oy + ty * C::BY, oz + z0 + pl);
+          if (g.p1 > 0)
+#ifdef LOPE_TMA_EVICT_LAST
+            lope_tma_load_2d_hint(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx,
+                                  by + (oz + z0 + pl) * g.p1);
+#else
+            lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx,
+                             by + (oz + z0 + pl) * g.p1);
+#endif
+          else
+            lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx, by, oz + z0 + pl);
         }
       }
     }
@@ -309,128 +403,193 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   }
 
   // ---------------- compute warps ----------------
-  const int wx = warp % BXW;
-  const int wy = warp / BXW;
-  const int col = wx * 32 + lane;          // column within the tile
+  const int wx = warp % WX;
+  const int wy = warp / WX;
+  const int cx = (wx * 32 + lane) * VX;    // first column of this lane within the tile
   const int row0 = wy * RY;                // first row within the tile
   const lope_i64 s1 = a.s1, s2 = a.s2;
-  const lope_i64 org0 = a.org - g.r0[0] - (lope_i64)g.r0[1] * s1 - (lope_i64)g.r0[2] * s2;
+  constexpr int SEC = 64 / (int)sizeof(T);          // one 64-byte DRAM atom
+  // The host sends only geometries with ext[0] % VX == 0 and, when images are
+  // refreshed, m[0] >= 2*SEC, m[0] % VX == 0 and m[d] >= lo[d] + hi[d] (each halo
+  // cell has exactly one image); anything else runs on the generic kernel.
+  const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
 
+  LopeUnitWalk w;
+  w.init(blockIdx.x, gridDim.x, nty, ntx);
   lope_u32 lbase = 0;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int ty = u % nty;
-    const int r_ = u / nty;
-    const int tx = r_ % ntx;
-    const int z0 = (r_ / ntx) * zc;
+  T hist[FZN > 0 ? FZN : 1][RY][VX];
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
+    const int z0 = w.zi * zc;
     const int nz = min(zc, g.ext[2] - z0);
-    const int x = tx * C::BX + col;
-    const int ybase = ty * C::BY + row0;
+    const int x = w.tx * C::BX + cx;
+    const int ybase = w.ty * C::BY + row0;
     const bool xok = x < g.ext[0];
-    // Periodic-image epilogue, precomputed per lane (x) / per warp row (y) / per plane
-    // (z): each dim has at most one image when m >= lo + hi; smaller interiors take
-    // the general (rare, slow) path.
-    // x images are written a whole 64-byte atom at a time: the SEC boundary lanes
-    // whose images land in the halo atom all store, padding cells included (the
-    // layout reserves an atom on each side), so no partial atoms reach DRAM.
-    constexpr int SEC = 64 / (int)sizeof(T);          // one 64-byte DRAM atom
+    const int nrow = min(RY, g.ext[1] - ybase);
+    // Periodic images (lope_step): x images are whole 64-byte atoms written by the
+    // lanes whose vectors land in the halo atom (padding included; the layout
+    // reserves an atom per side), y and z images are whole rows / planes.
     const int xg = x + g.r0[0];
-    const bool xw = (g.wrap & 1) && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
-    const int ximg = xg < SEC ? g.m[0] : -g.m[0];       // x image offset (if xw)
-    const bool one_x = g.m[0] >= 2 * SEC;
-    const bool one_y = g.m[1] >= g.lo[1] + g.hi[1];
-    const bool one_z = g.m[2] >= g.lo[2] + g.hi[2];
-    const bool simple = one_x && one_y && one_z;
-    // warp-uniform: does any lane of this warp have an x image, or any of its rows a y image?
-    const bool wx_any = __any_sync(0xffffffffu, xw && xok);
-    const bool wy_any = (g.wrap & 2) && (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
-                                         lope_near(min(ybase + RY - 1, g.ext[1] - 1) + g.r0[1], g.m[1],
-                                                   g.lo[1], g.hi[1]) ||
-                                         !one_y);
+    const bool xw = (g.wrap & 1) && xok && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
+    const int ximg = xg < SEC ? g.m[0] : -g.m[0];
+    const bool wx_any = __any_sync(0xffffffffu, xw);
+    const bool wy_any = (g.wrap & 2) && (nrow > 0) &&
+                        (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                         lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
     T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
     for (int pz = 0; pz < nz; ++pz, orow += s2) {
-      LopeSmemReader<T, C::BOXX, NZW, FZN> rd;
+      // ---- wait for the planes this iteration reads ----
+      const T* sp[NZW];
 #pragma unroll
-      for (int w = 0; w < NZW; ++w) {
-        const lope_u32 L = lbase + pz + w;
-        const lope_u32 slot = L % NS;
-        lope_mbar_wait(&full[slot], (L / NS) & 1);
-        rd.sp[w] = reinterpret_cast<const T*>(lope_smem + slot * C::STAGE_BYTES) +
-                   (row0 + Body::FN1) * C::BOXX + col + Body::FN0 + g.xshift;
+      for (int k = 0; k < NZW; ++k) {
+        const lope_u32 L = lbase + pz + k;
+        sp[k] = reinterpret_cast<const T*>(lope_smem + (L % NS) * C::STAGE_BYTES) + soff;
+        if (ZHIST && k < FZN && pz > 0) continue;          // past planes come from registers
+        lope_mbar_wait(&full[L % NS], (L / NS) & 1);
       }
-      T vals[RY];
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        LopeSmemReader<T, C::BOXX, NZW, FZN> rr;
-#pragma unroll
-        for (int w = 0; w < NZW; ++w) rr.sp[w] = rd.sp[w] + r * C::BOXX;
-        T res[1];
-        Body::template eval<T>(rr, sc.v, res);
-        vals[r] = res[0];
-      }
-      // every smem read of this plane is done: release the oldest slot (and, at the
-      // end of the unit, the trailing z-halo slots)
+#ifdef LOPE_DEBUG_NOCOMPUTE
       __syncwarp();
       if (lane == 0) {
         lope_mbar_arrive(&empty[(lbase + pz) % NS]);
         if (pz == nz - 1)
-          for (int w = 1; w < NZW; ++w) lope_mbar_arrive(&empty[(lbase + pz + w) % NS]);
+          for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
       }
-      if (!xok) continue;
-      const int zg = z0 + pz + g.r0[2];
-      const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
-      const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] : -(lope_i64)g.m[2]) * s2;
-      if (!(wy_any | zw) && simple) {
-        // no y/z images in this warp-plane: plain stores, plus the x-image sector store
-        // for the few boundary lanes
-        if (!wx_any) {
-#pragma unroll
-          for (int r = 0; r < RY; ++r)
-            if (ybase + r < g.ext[1]) orow[(lope_i64)r * s1] = vals[r];
-        } else {
-#pragma unroll
-          for (int r = 0; r < RY; ++r)
-            if (ybase + r < g.ext[1]) {
-              orow[(lope_i64)r * s1] = vals[r];
-#ifdef LOPE_XSAME
-              if (xw) orow[(lope_i64)r * s1] = vals[r];
-#else
-              if (xw) orow[(lope_i64)r * s1 + ximg] = vals[r];
-#endif
-            }
-        }
-      } else if (simple) {
+      if (xfull && nrow == RY) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
-          if (ybase + r >= g.ext[1]) continue;
+          V o;
+          T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) oe[e] = T(0);
+          *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
+        }
+      }
+      continue;
+#endif
+      // ---- register window ----
+      T win[NZW][NR][NXW];
+#pragma unroll
+      for (int k = 0; k < NZW; ++k) {
+        if (ZHIST && k < FZN) continue;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const T* rp = sp[k] + q * C::BOXX;
+          const V vv = *reinterpret_cast<const V*>(rp);
+          const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) win[k][q][Body::FN0 + e] = ve[e];
+#pragma unroll
+          for (int e = 1; e <= Body::FN0; ++e) win[k][q][Body::FN0 - e] = rp[-e];
+#pragma unroll
+          for (int e = 0; e < Body::FP0; ++e) win[k][q][Body::FN0 + VX + e] = rp[VX + e];
+        }
+      }
+      if (ZHIST && pz == 0) {
+        // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
+#pragma unroll
+        for (int d = 0; d < FZN; ++d) {
+          const lope_u32 L = lbase + (FZN - 1 - d);
+          lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            const V vv = *reinterpret_cast<const V*>(sp[FZN - 1 - d] + (Body::FN1 + r) * C::BOXX);
+            const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) hist[d][r][e] = ve[e];
+          }
+        }
+      }
+      // ---- evaluate ----
+      T vals[RY][VX];
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+#pragma unroll
+        for (int v = 0; v < VX; ++v) {
+          LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+          rd.win = &win[0][0][0];
+          rd.hist = &hist[0][0][0];
+          rd.r = r;
+          rd.v = v;
+          T res[1];
+          Body::template eval<T>(rd, sc.v, res);
+          vals[r][v] = res[0];
+        }
+      }
+      if (ZHIST) {
+#pragma unroll
+        for (int d = FZN - 1; d > 0; --d)
+#pragma unroll
+          for (int r = 0; r < RY; ++r)
+#pragma unroll
+            for (int e = 0; e < VX; ++e) hist[d][r][e] = hist[d - 1][r][e];
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int e = 0; e < VX; ++e) hist[0][r][e] = win[FZN][Body::FN1 + r][Body::FN0 + e];
+      }
+      // ---- release the slots no later plane of this unit needs ----
+      __syncwarp();
+      if (lane == 0) {
+        if (ZHIST) {
+          if (pz == 0)
+            for (int k = 0; k < FZN; ++k) lope_mbar_arrive(&empty[(lbase + k) % NS]);
+          lope_mbar_arrive(&empty[(lbase + pz + FZN) % NS]);
+          if (pz == nz - 1)
+            for (int k = 1; k <= FZP; ++k) lope_mbar_arrive(&empty[(lbase + pz + FZN + k) % NS]);
+        } else {
+          lope_mbar_arrive(&empty[(lbase + pz) % NS]);
+          if (pz == nz - 1)
+            for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
+        }
+      }
+      if (!xok || nrow <= 0) continue;
+      // ---- store ----
+      const int zg = z0 + pz + g.r0[2];
+      const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
+      if (!(wy_any | zw)) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          if (r >= nrow) continue;
+          V o;
+          T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+#ifdef LOPE_ST_EVICT_FIRST
+          lope_st_evict_first(orow + (lope_i64)r * s1, o);
+#else
+          *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
+#endif
+          if (wx_any && xw) *reinterpret_cast<V*>(orow + (lope_i64)r * s1 + ximg) = o;
+        }
+      } else {
+        const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] : -(lope_i64)g.m[2]) * s2;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          if (r >= nrow) continue;
+          V o;
+          T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
           T* p = orow + (lope_i64)r * s1;
-          const T v = vals[r];
-          p[0] = v;
-          if (xw) p[ximg] = v;
+          *reinterpret_cast<V*>(p) = o;
+          if (xw) *reinterpret_cast<V*>(p + ximg) = o;
           const int yg = ybase + r + g.r0[1];
           const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
           if (yw | zw) {
             const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] : -(lope_i64)g.m[1]) * s1;
             if (yw) {
-              p[yimg] = v;
-              if (xw) p[yimg + ximg] = v;
+              *reinterpret_cast<V*>(p + yimg) = o;
+              if (xw) *reinterpret_cast<V*>(p + yimg + ximg) = o;
             }
             if (zw) {
-              p[zimg] = v;
-              if (xw) p[zimg + ximg] = v;
+              *reinterpret_cast<V*>(p + zimg) = o;
+              if (xw) *reinterpret_cast<V*>(p + zimg + ximg) = o;
               if (yw) {
-                p[zimg + yimg] = v;
-                if (xw) p[zimg + yimg + ximg] = v;
+                *reinterpret_cast<V*>(p + zimg + yimg) = o;
+                if (xw) *reinterpret_cast<V*>(p + zimg + yimg + ximg) = o;
               }
             }
           }
         }
-      } else {
-#pragma unroll
-        for (int r = 0; r < RY; ++r)
-          if (ybase + r < g.ext[1]) {
-            orow[(lope_i64)r * s1] = vals[r];
-            lope_store_images<T>(a.out, s1, s2, org0, xg, ybase + r + g.r0[1], zg, g, vals[r]);
-          }
       }
     }
     lbase += nz + NZW - 1;

@@ -12,6 +12,9 @@ if name == "copy3d":
 elif name == "copy3dh":
     from paper_1502_03504_b200.ir import KernelBuilder
     kb = KernelBuilder("copy3dh", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0] + 0 * (u[1, 1, 0] + u[-1, -1, 0])); kir = kb.build()
+elif name == "copy2dh":
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder("copy2dh", 2); u = kb.array("u"); kb.store(u, u[0, 0] + 0 * (u[1, 1] + u[-1, -1])); kir = kb.build()
 elif name == "copy3dz":
     from paper_1502_03504_b200.ir import KernelBuilder
     kb = KernelBuilder("copy3dz", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0] + 0 * (u[0, 0, 1] + u[0, 0, -1])); kir = kb.build()
