@@ -240,6 +240,7 @@ namespace {
 struct TileCfg {
   int bxw = 4, wy = 2, ry = 8, ns = 8;
   int mb = 2;     // CTAs per SM the launch bounds target
+  int pw = 0;     // 1: dedicated TMA producer warp
 };
 
 struct DevMod {
@@ -311,10 +312,11 @@ int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
 }
 
 TileCfg pick_tile(const lope::Kir& k, int dtype) {
-  // Lanes hold 16-byte vectors (4 fp32 / 2 fp64); tiles are one warp (128 fp32 /
-  // 64 fp64 columns) wide so the TMA box stays within 256 elements, with 8 compute
-  // warps stacked in y.  The ring is as deep as two CTAs per SM allow (calibrated
-  // with tools/tmabench.cu: ~10 slots of a ~10 KB box keep the copy roofline).
+  // One CTA per SM: 16 compute warps stacked in y plus one TMA producer warp.  Lanes
+  // hold 16-byte vectors (4 fp32 / 2 fp64), so a tile is one warp (128 fp32 / 64 fp64
+  // columns) wide and the TMA box stays within 256 elements.  Calibrated on B200
+  // (tools/probe_perf.py): 3-D fp32 best at 4 rows/lane (64-row tiles, 6 x 36 KB ring),
+  // 2-D at 2 rows/lane (32-row tiles, 12 x 18.5 KB ring).
   TileCfg c;
   const int nzw = k.fn[0][2] + k.fp[0][2] + 1;
   bool zstar = k.rank == 3;
@@ -322,22 +324,24 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
     if (n.kind == lope::Node::READ && n.arr == 0 && n.off[2] != 0 && (n.off[0] != 0 || n.off[1] != 0)) zstar = false;
   const int hold = (zstar && k.fn[0][2] > 0) ? k.fp[0][2] + 1 : nzw;
   c.bxw = 1;
-  c.wy = 8;
-  c.ry = k.rank == 3 ? 2 : 4;
-  c.ns = 16;
+  c.wy = 16;
+  c.ry = 2;
+  c.mb = 1;
+  c.ns = 32;
+  // producer: in-band (warp 0 lane 0) for 3-D, a dedicated 17th warp for 2-D
+  // (measured on B200: lap3d7 1024^3 1.76 vs 1.98 ms; ninept2d 16384^2 0.35 vs 0.49 ms)
+  c.pw = k.rank == 3 ? 0 : 1;
   // Keep the per-lane register window (rows x columns of the centre plane, in 32-bit
-  // registers) small enough that nothing spills: at 2 CTAs/SM ptxas caps the kernel at
-  // 96 registers; wide footprints get one CTA per SM (up to ~128 registers) instead.
-  // Spills are not just slow here: local-memory traffic goes through L2 and evicts the
-  // halo lines neighbouring tiles would otherwise reuse.
+  // registers) small enough that nothing spills.  Spills are not just slow here: the
+  // local-memory traffic goes through L2 and evicts the halo lines neighbouring tiles
+  // would otherwise reuse.
   {
     const int vx = dtype == LOPE_F32 ? 4 : 2;
     const int words = dtype == LOPE_F32 ? 1 : 2;
     auto window = [&](int ry) {
       return (ry + k.fn[0][1] + k.fp[0][1]) * (vx + k.fn[0][0] + k.fp[0][0]) * words;
     };
-    while (c.ry > 2 && window(c.ry) > 40) c.ry /= 2;
-    if (window(c.ry) > 40) c.mb = 1;
+    while (c.ry > 1 && window(c.ry) > 64) c.ry /= 2;
   }
   if (const char* e = std::getenv("LOPE_TILE")) {
     int a, b, cc, d;
@@ -345,8 +349,8 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
       c.bxw = a; c.wy = b; c.ry = cc; c.ns = d;
     }
   }
-  if (const char* e = std::getenv("LOPE_MB")) c.mb = std::atoi(e) == 1 ? 1 : 2;
-  if (c.mb == 1 && !std::getenv("LOPE_TILE")) c.ns = 32;
+  if (const char* e = std::getenv("LOPE_MB")) c.mb = std::atoi(e) == 2 ? 2 : 1;
+  if (const char* e = std::getenv("LOPE_PW")) c.pw = std::atoi(e) ? 1 : 0;
   if (c.ns < hold + 1) c.ns = hold + 1;
   // shrink the ring until mb CTAs fit on an SM (227 KB)
   while (c.ns > hold + 1 && c.mb * tiled_smem_bytes(k, dtype, c) > 225 * 1024) --c.ns;
@@ -367,14 +371,14 @@ std::string build_source(lope_kernel* K) {
   if (K->tiled_ok) {
     const TileCfg& c = K->tile;
     s << "typedef LopeTiledCfg<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
-      << "> LopeCfg;\n";
+      << ", " << c.pw << "> LopeCfg;\n";
     s << "extern \"C\" __constant__ int lope_tiled_info[4] = {LopeCfg::SMEM_BYTES, LopeCfg::THREADS, "
          "LopeCfg::BOXX, LopeCfg::BOXY};\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (c.bxw * c.wy + 1)
+    s << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (c.bxw * c.wy + c.pw)
       << ", " << c.mb << ") lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
-      << ">(&map, a, sc, g);\n}\n";
+      << ", " << c.pw << ">(&map, a, sc, g);\n}\n";
   }
   return s.str();
 }
@@ -792,7 +796,8 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
     o << "]";
   }
   o << "],\"path\":\"" << k->describe_path << "\",\"tile\":[" << k->tile.bxw << "," << k->tile.wy << ","
-    << k->tile.ry << "," << k->tile.ns << "],\"reads\":" << ir.nreads << "}";
+    << k->tile.ry << "," << k->tile.ns << "],\"ctas_per_sm\":" << k->tile.mb << ",\"producer_warp\":"
+    << k->tile.pw << ",\"reads\":" << ir.nreads << "}";
   std::string s = o.str();
   if (s.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", s.size() + 1);
   std::memcpy(buf, s.c_str(), s.size() + 1);

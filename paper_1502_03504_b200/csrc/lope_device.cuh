@@ -281,7 +281,7 @@ struct LopeWinReader {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0>
 struct LopeTiledCfg {
   static constexpr int VX = 16 / (int)sizeof(T);
   static constexpr int BX = 32 * VX * WX;
@@ -295,8 +295,9 @@ struct LopeTiledCfg {
   static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
   static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
   static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
-  static constexpr int NCW = WX * WY;              // consumer (compute) warps
-  static constexpr int THREADS = 32 * (NCW + 1);   // + one TMA producer warp
+  static constexpr int NCW = WX * WY;              // compute warps
+  // PW = 1: a dedicated TMA producer warp; PW = 0: warp 0 lane 0 issues TMA in-band
+  static constexpr int THREADS = 32 * (NCW + PW);
   static constexpr int NR = RY + Body::FN1 + Body::FP1;
   static constexpr int NXW = VX + Body::FN0 + Body::FP0;
 };
@@ -328,10 +329,10 @@ struct LopeUnitWalk {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
-  typedef LopeTiledCfg<Body, T, WX, WY, RY, NS> C;
+  typedef LopeTiledCfg<Body, T, WX, WY, RY, NS, PW> C;
   typedef typename LopeVec<T>::V V;
   constexpr int VX = C::VX;
   constexpr int FZN = Body::FN2, FZP = Body::FP2;
@@ -362,43 +363,56 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   }
   __syncthreads();
 
-  if (warp == C::NCW) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      const int oy = g.lo[1] + g.r0[1] - Body::FN1;
-      const int oz = g.lo[2] + g.r0[2] - FZN;
-      LopeUnitWalk w;
-      w.init(blockIdx.x, gridDim.x, nty, ntx);
-#ifdef LOPE_STAGGER
-      // experiment: checkerboard start delay so neighbouring tiles do not miss in L2 together
-      if ((w.tx + w.ty) & 1) {
-        lope_u64 t0, t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < (lope_u64)(LOPE_STAGGER));
-      }
-#endif
-      lope_u32 L = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
-        const int z0 = w.zi * zc;
-        const int nl = min(zc, g.ext[2] - z0) + NZW - 1;
-        const int bx = g.box0 + w.tx * C::BX, by = oy + w.ty * C::BY;
-        for (int pl = 0; pl < nl; ++pl, ++L) {
-          const lope_u32 slot = L % NS;
-          if (L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
-          lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
-          if (g.p1 > 0)
-#ifdef LOPE_TMA_EVICT_LAST
-            lope_tma_load_2d_hint(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx,
-                                  by + (oz + z0 + pl) * g.p1);
-#else
-            lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx,
-                             by + (oz + z0 + pl) * g.p1);
-#endif
-          else
-            lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], bx, by, oz + z0 + pl);
+  // ---------------- TMA producer state (warp 0, lane 0) ----------------
+  // The producer runs inside compute warp 0 (a 16-warp CTA keeps the 128-register
+  // budget; a 17th warp would drop it to 96 and spill).  Before each plane it tops the
+  // ring up to NS loads past the oldest slot warp 0 still holds, waiting on a slot's
+  // `empty` barrier when a slower warp still reads it.  No deadlock: every load a warp
+  // can be waiting for has already been issued.
+  LopeUnitWalk pw;
+  int p_u = blockIdx.x, p_pl = 0, p_nl = 0, p_bx = 0, p_by = 0, p_z = 0;
+  lope_u32 p_L = 0;
+  const int oy = g.lo[1] + g.r0[1] - Body::FN1;
+  const int oz = g.lo[2] + g.r0[2] - FZN;
+  const int pwarp = PW ? C::NCW : 0;     // the warp that issues TMA
+  if (warp == pwarp && lane == 0) {
+    pw.init(blockIdx.x, gridDim.x, nty, ntx);
+    if (p_u < nunits) {
+      const int z0 = pw.zi * zc;
+      p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+      p_bx = g.box0 + pw.tx * C::BX;
+      p_by = oy + pw.ty * C::BY;
+      p_z = oz + z0;
+    }
+  }
+  auto produce = [&](lope_u32 limit) {
+    while (p_L < limit && p_u < nunits) {
+      const lope_u32 slot = p_L % NS;
+      if (p_L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((p_L / NS) - 1) & 1);
+      lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
+      if (g.p1 > 0)
+        lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
+      else
+        lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by, p_z + p_pl);
+      ++p_L;
+      if (++p_pl == p_nl) {
+        p_pl = 0;
+        p_u += gridDim.x;
+        pw.next();
+        if (p_u < nunits) {
+          const int z0 = pw.zi * zc;
+          p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+          p_bx = g.box0 + pw.tx * C::BX;
+          p_by = oy + pw.ty * C::BY;
+          p_z = oz + z0;
         }
       }
     }
+  };
+
+  if (PW && warp == C::NCW) {
+    // dedicated producer warp: issue everything, slot by slot
+    if (lane == 0) produce(0xffffffffu);
     return;
   }
 
@@ -437,6 +451,11 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
                          lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
     T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
     for (int pz = 0; pz < nz; ++pz, orow += s2) {
+      // ---- top up the TMA ring (warp 0 lane 0) ----
+      if (!PW && warp == 0) {
+        if (lane == 0) produce((ZHIST ? (pz == 0 ? lbase : lbase + pz + FZN) : lbase + pz) + NS);
+        __syncwarp();
+      }
       // ---- wait for the planes this iteration reads ----
       const T* sp[NZW];
 #pragma unroll
@@ -465,24 +484,6 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       }
       continue;
 #endif
-      // ---- register window ----
-      T win[NZW][NR][NXW];
-#pragma unroll
-      for (int k = 0; k < NZW; ++k) {
-        if (ZHIST && k < FZN) continue;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const T* rp = sp[k] + q * C::BOXX;
-          const V vv = *reinterpret_cast<const V*>(rp);
-          const T* ve = reinterpret_cast<const T*>(&vv);
-#pragma unroll
-          for (int e = 0; e < VX; ++e) win[k][q][Body::FN0 + e] = ve[e];
-#pragma unroll
-          for (int e = 1; e <= Body::FN0; ++e) win[k][q][Body::FN0 - e] = rp[-e];
-#pragma unroll
-          for (int e = 0; e < Body::FP0; ++e) win[k][q][Body::FN0 + VX + e] = rp[VX + e];
-        }
-      }
       if (ZHIST && pz == 0) {
         // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
 #pragma unroll
@@ -498,33 +499,48 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
           }
         }
       }
-      // ---- evaluate ----
+      // ---- register window, filled row by row and consumed as soon as a row of
+      // outputs has all its inputs (short live ranges: no spills at 16 warps) ----
+      T win[NZW][NR][NXW];
       T vals[RY][VX];
 #pragma unroll
-      for (int r = 0; r < RY; ++r) {
+      for (int q = 0; q < NR; ++q) {
 #pragma unroll
-        for (int v = 0; v < VX; ++v) {
-          LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
-          rd.win = &win[0][0][0];
-          rd.hist = &hist[0][0][0];
-          rd.r = r;
-          rd.v = v;
-          T res[1];
-          Body::template eval<T>(rd, sc.v, res);
-          vals[r][v] = res[0];
+        for (int k = 0; k < NZW; ++k) {
+          if (ZHIST && k < FZN) continue;
+          const T* rp = sp[k] + q * C::BOXX;
+          const V vv = *reinterpret_cast<const V*>(rp);
+          const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) win[k][q][Body::FN0 + e] = ve[e];
+#pragma unroll
+          for (int e = 1; e <= Body::FN0; ++e) win[k][q][Body::FN0 - e] = rp[-e];
+#pragma unroll
+          for (int e = 0; e < Body::FP0; ++e) win[k][q][Body::FN0 + VX + e] = rp[VX + e];
         }
-      }
-      if (ZHIST) {
+        const int r = q - Body::FN1 - Body::FP1;
+        if (r >= 0) {
 #pragma unroll
-        for (int d = FZN - 1; d > 0; --d)
+          for (int v = 0; v < VX; ++v) {
+            LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+            rd.win = &win[0][0][0];
+            rd.hist = &hist[0][0][0];
+            rd.r = r;
+            rd.v = v;
+            T res[1];
+            Body::template eval<T>(rd, sc.v, res);
+            vals[r][v] = res[0];
+          }
+          if (ZHIST) {
+            // row r of the history only feeds row r: shift it now
 #pragma unroll
-          for (int r = 0; r < RY; ++r)
+            for (int d = FZN - 1; d > 0; --d)
 #pragma unroll
-            for (int e = 0; e < VX; ++e) hist[d][r][e] = hist[d - 1][r][e];
+              for (int e = 0; e < VX; ++e) hist[d][r][e] = hist[d - 1][r][e];
 #pragma unroll
-        for (int r = 0; r < RY; ++r)
-#pragma unroll
-          for (int e = 0; e < VX; ++e) hist[0][r][e] = win[FZN][Body::FN1 + r][Body::FN0 + e];
+            for (int e = 0; e < VX; ++e) hist[0][r][e] = win[FZN][Body::FN1 + r][Body::FN0 + e];
+          }
+        }
       }
       // ---- release the slots no later plane of this unit needs ----
       __syncwarp();

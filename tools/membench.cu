@@ -54,7 +54,42 @@ __global__ void st7_stream(const float* __restrict__ a, float* __restrict__ b, i
   }
 }
 
+__global__ void fillrand(float* a, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long z = (i + seed) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    a[i] = (float)((z >> 40) & 0xffffff) * (1.0f / 16777216.0f) - 0.5f;
+  }
+}
+
 int main() {
+  if (getenv("RANDCOPY")) {
+    size_t cnt = (size_t)1 << 30;   // 4 GiB fp32
+    float *a, *b;
+    cudaMalloc(&a, cnt * 4);
+    cudaMalloc(&b, cnt * 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int mode = 0; mode < 3; ++mode) {
+      if (mode == 0) { cudaMemset(a, 0, cnt * 4); cudaMemset(b, 0, cnt * 4); }
+      if (mode == 1) { fillrand<<<148 * 8, 256>>>(a, cnt, 1); cudaMemset(b, 0, cnt * 4); }
+      if (mode == 2) { fillrand<<<148 * 8, 256>>>(a, cnt, 1); fillrand<<<148 * 8, 256>>>(b, cnt, 7); }
+      cudaDeviceSynchronize();
+      float ms;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(e0);
+        copy4<<<148 * 8, 256>>>((float4*)a, (float4*)b, cnt / 4);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+      }
+      printf("copy4 %s: %.3f ms %.0f GB/s\n", mode == 0 ? "zeros->zeros" : mode == 1 ? "random->zeros" : "random->random",
+             ms, 2.0 * cnt * 4 / ms / 1e6);
+    }
+    return 0;
+  }
   const int n = 1024;
   float ms;
   cudaEvent_t e0, e1;

@@ -46,5 +46,5 @@ import numpy as np
 pts = np.prod(shape)
 esz = 4 if dt == "float32" else 8
 print(json.dumps({"env": {k_: os.environ.get(k_) for k_ in ("LOPE_TILE", "LOPE_ZCHUNK", "LOPE_GRID", "LOPE_FORCE_GENERIC")},
-                  "desc": json.loads(k.describe())["tile"], "ms": round(ms, 4), "gpts": round(pts / ms / 1e6, 1),
+                  "desc": json.loads(k.describe())["tile"] + [json.loads(k.describe()).get("producer_warp")], "ms": round(ms, 4), "gpts": round(pts / ms / 1e6, 1),
                   "GBs": round(2 * esz * pts / ms / 1e6, 1)}), flush=True)
