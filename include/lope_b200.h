@@ -99,6 +99,14 @@ int lope_launch(const lope_kernel* k, const lope_layout* layouts, const int64_t*
 int lope_step(const lope_kernel* k, const lope_layout* layout, const void* in, void* out,
               const double* rscal, const int64_t* iscal, int32_t wrap_mask, void* stream);
 
+/* lope_step restricted to interior planes [begin, end) of the slowest dimension (0-based,
+ * half-open): the slab-decomposed pipeline computes boundary planes first, exchanges
+ * them, and computes the interior planes meanwhile.  Images are refreshed only along
+ * wrap_mask dims (the decomposed dim is left to the exchange). */
+int lope_step_planes(const lope_kernel* k, const lope_layout* layout, const void* in, void* out,
+                     int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
+                     int32_t wrap_mask, void* stream);
+
 /* _halo_exchange with every neighbour equal to self along the dims in dims_mask:
  * each halo cell gets its periodic image (in place).  E108 if a halo is wider
  * than the interior. */

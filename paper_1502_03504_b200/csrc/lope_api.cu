@@ -873,6 +873,14 @@ int lope_launch(const lope_kernel* kc, const lope_layout* layouts, const int64_t
 
 int lope_step(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
               const double* rscal, const int64_t* iscal, int32_t wrap_mask, void* stream) {
+  if (!layout) return fail(108, "null argument");
+  return lope_step_planes(kc, layout, in, out, 0, layout->interior[layout->rank - 1], rscal, iscal,
+                          wrap_mask, stream);
+}
+
+int lope_step_planes(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
+                     int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
+                     int32_t wrap_mask, void* stream) {
   lope_kernel* k = const_cast<lope_kernel*>(kc);
   if (!k || !layout) return fail(108, "null argument");
   if (int e = check_layout(layout)) return e;
@@ -886,8 +894,15 @@ int lope_step(const lope_kernel* kc, const lope_layout* layout, const void* in, 
     if (ir.fn[0][d] > layout->lo[d] || ir.fp[0][d] > layout->hi[d])
       return fail(102, "kernel '%s' footprint exceeds the halo in dim %d", ir.name.c_str(), d + 1);
   if (int e = check_interior_halo(layout)) return e;
+  const int sd = layout->rank - 1;   // slowest dimension
+  if (begin < 0 || end > layout->interior[sd] || begin > end)
+    return fail(108, "plane range %lld:%lld outside 0:%lld", (long long)begin, (long long)end,
+                (long long)layout->interior[sd]);
+  if (begin == end) return 0;
   int r0[3] = {0, 0, 0}, ext[3];
   for (int d = 0; d < 3; ++d) ext[d] = (int)layout->interior[d];
+  r0[sd] = (int)begin;
+  ext[sd] = (int)(end - begin);
   const void* ins[1] = {in};
   void* outs[1] = {out};
   int wrap = wrap_mask & ((1 << ir.rank) - 1);
