@@ -271,6 +271,11 @@ def run_gpu_arm(args, wl):
     for _ in range(args.warmup):
         do_step()
     torch.cuda.synchronize()
+    graph = None
+    if ws == 1 and points * esz < 64 << 20:
+        # L2-resident field (config 1): launch-bound, so the K timed steps are captured
+        # once as a CUDA graph (after the plain warm-up steps) and replayed once
+        graph = R.StepGraph(kern, arr, args.steps)
 
     def barrier():
         if ws > 1:
@@ -286,23 +291,31 @@ def run_gpu_arm(args, wl):
     barrier()
     with ClockSampler(local) as clk:
         t_all0.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            do_step()
-            ev[i][1].record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                ev[i][0].record(stream)
+                do_step()
+                ev[i][1].record(stream)
         t_all1.record(stream)
         torch.cuda.synchronize()
+    steps_done = graph.steps if graph is not None else args.steps
     barrier()
     launches = _lib.launch_count() - l0
     total_ms = t_all0.elapsed_time(t_all1)
-    per_step = [a.elapsed_time(b) for a, b in ev]
+    if graph is not None:
+        launches = steps_done          # one graph replay: the host counter saw the captures
+        per_step = [total_ms / steps_done]
+    else:
+        per_step = [a.elapsed_time(b) for a, b in ev]
     if ws > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = points * ws * args.steps / (total_ms / 1e3) / 1e9
+    ms_per_step = total_ms / steps_done
+    value = points * ws * steps_done / (total_ms / 1e3) / 1e9
 
     # dominant kernel: the fused step kernel, one launch per step at N=1
     kernel_ms = sorted(per_step)[len(per_step) // 2] if ws == 1 else None
@@ -331,6 +344,7 @@ def run_gpu_arm(args, wl):
         line = {
             "metric": "stencil Gpoints/s & HBM GB/s (% of 8 TB/s roofline) at 1/2/4/8 B200 vs CPU ref",
             "value": round(value, 3), "unit": "Gpoints/s", "n_gpus": ws, "steps": args.steps,
+            "cuda_graph": graph is not None,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if wl["dtype"] == "float32" else "f64",
