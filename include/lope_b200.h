@@ -117,6 +117,19 @@ int lope_halo_fill(const lope_layout* layout, void* buf, int32_t dims_mask, void
 int lope_pack(const lope_layout* layout, const void* host, void* dev, void* stream);
 int lope_unpack(const lope_layout* layout, const void* dev, void* host, void* stream);
 
+/* Same for the whole padded block (halo cells included): the host side is exactly
+ * the reference's flat column-major block (DistributedArray.blocks[k],
+ * runtime.py:471). */
+int lope_pack_padded(const lope_layout* layout, const void* host, void* dev, void* stream);
+int lope_unpack_padded(const lope_layout* layout, const void* dev, void* host, void* stream);
+
+/* dst[box at dst_lo] := src[box at src_lo] for two blocks of the same layout; boxes of
+ * `extent` cells in padded coordinates (3 entries each).  The halo slabs of
+ * _halo_exchange between images and the device-mirror pulls / pushes
+ * (runtime.py:669-711) are such boxes.  E108 if a box leaves the padded block. */
+int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const int64_t* dst_lo,
+                  const int64_t* src_lo, const int64_t* extent, void* stream);
+
 /* Fill the interior with the synthetic U(-1,1) field: value of global cell
  * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
  * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */

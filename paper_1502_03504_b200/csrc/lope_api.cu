@@ -206,6 +206,24 @@ __global__ void __launch_bounds__(256) lope_k_copy_through(const T* __restrict__
   }
 }
 
+// dst[box at dlo] := src[box at slo], boxes of extent e (padded coordinates, same layout).
+template <class T>
+__global__ void __launch_bounds__(256) lope_k_copy_box(T* __restrict__ dst, const T* __restrict__ src,
+                                                       DevLayout L, long long d0, long long d1, long long d2,
+                                                       long long s0, long long s1, long long s2, long long e0,
+                                                       long long e1, long long e2) {
+  const long long nrows = e1 * e2;
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < nrows; r += nw) {
+    const long long j = r % e1, k = r / e1;
+    T* drow = dst + L.B + d0 + (d1 + j) * L.S1 + (d2 + k) * L.S2;
+    const T* srow = src + L.B + s0 + (s1 + j) * L.S1 + (s2 + k) * L.S2;
+    for (long long x = lane; x < e0; x += 32) drow[x] = srow[x];
+  }
+}
+
 __device__ __forceinline__ unsigned long long lope_splitmix64(unsigned long long x) {
   unsigned long long z = x + 0x9E3779B97F4A7C15ULL;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -931,17 +949,21 @@ int lope_halo_fill(const lope_layout* layout, void* buf, int32_t dims_mask, void
   return 0;
 }
 
-static int pack_impl(const lope_layout* L, const void* host, void* dev, cudaStream_t st, bool to_dev) {
+static int pack_impl(const lope_layout* L, const void* host, void* dev, cudaStream_t st, bool to_dev,
+                     bool padded = false) {
   if (int e = check_layout(L)) return e;
   if (!host || !dev) return fail(202, "null buffer");
   cudaMemcpy3DParms p;
   std::memset(&p, 0, sizeof p);
   const size_t eb = (size_t)L->elem_bytes;
-  cudaPitchedPtr hp = make_cudaPitchedPtr(const_cast<void*>(host), L->interior[0] * eb, L->interior[0],
-                                          L->interior[1]);
+  // host side: the interior (or, with `padded`, the whole padded block) packed
+  // column-major exactly like the reference's flat blocks (ir.py:189-230)
+  const int64_t* hx = padded ? L->padded : L->interior;
+  cudaPitchedPtr hp = make_cudaPitchedPtr(const_cast<void*>(host), hx[0] * eb, hx[0], hx[1]);
   cudaPitchedPtr dp = make_cudaPitchedPtr(dev, L->stride[1] * eb, L->stride[1], L->padded[1]);
-  cudaPos dpos = make_cudaPos((L->base + L->lo[0]) * eb, L->lo[1], L->lo[2]);
-  p.extent = make_cudaExtent(L->interior[0] * eb, L->interior[1], L->interior[2]);
+  cudaPos dpos = padded ? make_cudaPos(L->base * eb, 0, 0)
+                        : make_cudaPos((L->base + L->lo[0]) * eb, L->lo[1], L->lo[2]);
+  p.extent = make_cudaExtent(hx[0] * eb, hx[1], hx[2]);
   if (to_dev) {
     p.srcPtr = hp;
     p.dstPtr = dp;
@@ -963,6 +985,44 @@ int lope_pack(const lope_layout* layout, const void* host, void* dev, void* stre
 
 int lope_unpack(const lope_layout* layout, const void* dev, void* host, void* stream) {
   return pack_impl(layout, host, const_cast<void*>(dev), (cudaStream_t)stream, false);
+}
+
+int lope_pack_padded(const lope_layout* layout, const void* host, void* dev, void* stream) {
+  return pack_impl(layout, host, dev, (cudaStream_t)stream, true, true);
+}
+
+int lope_unpack_padded(const lope_layout* layout, const void* dev, void* host, void* stream) {
+  return pack_impl(layout, host, const_cast<void*>(dev), (cudaStream_t)stream, false, true);
+}
+
+int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const int64_t* dst_lo,
+                  const int64_t* src_lo, const int64_t* extent, void* stream) {
+  if (int e = check_layout(layout)) return e;
+  if (!dst || !src || !dst_lo || !src_lo || !extent) return fail(202, "null argument");
+  for (int d = 0; d < 3; ++d) {
+    if (extent[d] < 0 || dst_lo[d] < 0 || src_lo[d] < 0 || dst_lo[d] + extent[d] > layout->padded[d] ||
+        src_lo[d] + extent[d] > layout->padded[d])
+      return fail(108, "box outside the padded block in dim %d", d + 1);
+    if (extent[d] == 0) return 0;
+  }
+  DevLayout d = dev_layout(layout);
+  cudaStream_t st = (cudaStream_t)stream;
+  long long rows = extent[1] * extent[2];
+  long long blocks = (rows * 32 + 255) / 256;
+  long long cap = (long long)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (layout->dtype == LOPE_F32)
+    lope_k_copy_box<float><<<(int)blocks, 256, 0, st>>>((float*)dst, (const float*)src, d, dst_lo[0], dst_lo[1],
+                                                         dst_lo[2], src_lo[0], src_lo[1], src_lo[2], extent[0],
+                                                         extent[1], extent[2]);
+  else
+    lope_k_copy_box<double><<<(int)blocks, 256, 0, st>>>((double*)dst, (const double*)src, d, dst_lo[0],
+                                                          dst_lo[1], dst_lo[2], src_lo[0], src_lo[1], src_lo[2],
+                                                          extent[0], extent[1], extent[2]);
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return 0;
 }
 
 int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const int64_t* gext,

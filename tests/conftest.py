@@ -51,3 +51,29 @@ def golden_random():
 @pytest.fixture(scope="session")
 def golden_kats():
     return load_json("kats.json")
+
+
+def import_lopec(allow_reference_tree: bool = False):
+    """Import the reference package for the Machine drop-in tests.
+
+    The drop-in keeps lopec's frontend and host plan, so its tests need lopec
+    itself: the copy installed under baseline/_ref (which travels to the GPU box)
+    or, in the build container only, the read-only reference tree.
+    """
+    try:
+        import lopec  # noqa: F401
+        return True
+    except ImportError:
+        pass
+    cands = [REPO / "baseline" / "_ref"]
+    if allow_reference_tree:
+        cands.append(pathlib.Path("/root/reference/pkg/src"))
+    for c in cands:
+        if (c / "lopec" / "__init__.py").exists():
+            sys.path.insert(0, str(c))
+            try:
+                import lopec  # noqa: F401
+                return True
+            except ImportError:
+                sys.path.remove(str(c))
+    return False

@@ -387,6 +387,95 @@ end program main
     (HERE / "kats.json").write_text(json.dumps(kats, indent=1) + "\n")
 
 
+# Programs for the Machine drop-in tests: written here (not copied from the corpus),
+# each with a device subimage so the mirror path and its counters are exercised.
+MACHINE_MAIN = """\
+{kernel}
+program main
+  real, allocatable, dimension({dims}), codimension[{codims}], HALO({halo}) :: U
+  integer :: device
+  integer :: it
+  device = GET_SUBIMAGE({sub})
+  allocate(U({bounds})[{cob}])
+  if (device /= this_image()) then
+    allocate(U[device], HALO_SRC=U) [[device]]
+  end if
+  do it = 1, nsteps
+    call HALO_TRANSFER(U, BC=CYCLIC)
+    do concurrent ({conc}) [[device]]
+      call {kname}( U({idx})[device]{extra} )
+    end do
+  end do
+  if (device /= this_image()) then
+    U = U[device]
+  end if
+end program main
+"""
+
+MACHINE_KERNELS = {
+    "fig1": ("""\
+pure concurrent subroutine fig1(U)
+  real, dimension(:,:), HALO(:,:) :: U
+  U(0,0) = U(0,+1) + U(-1,0) - 3*U(0,0) + U(+1,0) + U(0,-1)
+end subroutine fig1
+""", 2, (1, 1, 1, 1), ""),
+    "mean3": ("""\
+pure concurrent subroutine mean3(A)
+  real, dimension(:), HALO(:) :: A
+  A(0) = (A(-1) + A(0) + A(+1)) / 3
+end subroutine mean3
+""", 1, (1, 1), ""),
+    "skew": ("""\
+pure concurrent subroutine skew(U, c)
+  real, dimension(:,:), HALO(:,:) :: U
+  real :: c
+  real :: t
+  t = U(-1,0) - U(-2,0)
+  U(0,0) = U(0,0) + c*t + 0.125*(U(0,-1) - 2*U(0,0) + U(0,+1))
+end subroutine skew
+""", 2, (2, 0, 1, 1), ", 0.25"),
+}
+
+
+def machine_program(kname, sub=1):
+    src, rank, w, extra = MACHINE_KERNELS[kname]
+    if rank == 1:
+        l0, h0 = w
+        return MACHINE_MAIN.format(kernel=src, dims=":", codims=":", halo=f"{l0}:*:{h0}", sub=sub,
+                                   bounds=f"{1 - l0}:M+{h0}", cob="*", conc="i=1:M", kname=kname,
+                                   idx="i", extra=extra)
+    l0, h0, l1, h1 = w
+    return MACHINE_MAIN.format(kernel=src, dims=":,:", codims=":,:", halo=f"{l0}:*:{h0}, {l1}:*:{h1}",
+                               sub=sub, bounds=f"{1 - l0}:M+{h0}, {1 - l1}:N+{h1}", cob="MP,*",
+                               conc="i=1:M, j=1:N", kname=kname, idx="i,j", extra=extra)
+
+
+def gen_machine():
+    rng = np.random.default_rng(777)
+    cases = []
+    arrays = {}
+    for kname, shape, runs in (
+            ("fig1", (8, 8), [(1, 1, 0, 3), (2, 1, 0, 3), (4, 2, 1, 2), (2, 2, 1, 2), (1, 1, 1, 1)]),
+            ("mean3", (24, 1), [(1, 1, 0, 4), (4, 1, 1, 3)]),
+            ("skew", (12, 8), [(1, 1, 1, 3), (2, 2, 0, 2), (4, 4, 1, 2)])):
+        text = machine_program(kname)
+        result = compile_text(text)
+        field = rng.uniform(-1, 1, shape)
+        for images, rows, devices, steps in runs:
+            m = run_machine(result, field.copy(), images=images, grid_rows=rows, devices=devices, steps=steps)
+            tag = f"{kname}_p{images}_r{rows}_d{devices}_k{steps}"
+            arrays[tag + "_in"] = field
+            arrays[tag + "_out"] = m.gather()
+            for k in m.images:
+                arrays[f"{tag}_blk{k}"] = m.arrays["u"].view(k).copy()
+            cases.append({"tag": tag, "kernel": kname, "images": images, "grid_rows": rows,
+                          "devices": devices, "steps": steps, "text": text,
+                          "counters": {str(k): v for k, v in m.counters.items()},
+                          "events": [list(e) for e in m.events]})
+    np.savez_compressed(HERE / "machine.npz", **arrays)
+    (HERE / "machine.json").write_text(json.dumps(cases, indent=1) + "\n")
+
+
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
     gen_kernels()
@@ -394,5 +483,6 @@ if __name__ == "__main__":
     gen_exchange()
     gen_random()
     gen_kats()
+    gen_machine()
     for p in sorted(HERE.iterdir()):
         print(p.name, p.stat().st_size)

@@ -107,3 +107,15 @@ def test_compiled_kernel_object_without_gpu():
         assert rs[0] == 0.25
     with pytest.raises(RuntimeFault):
         k.scalar_args({})
+
+
+def test_machine_dropin_subclasses_the_reference_machine():
+    from conftest import import_lopec
+    if not import_lopec(allow_reference_tree=True):
+        pytest.skip("lopec not importable")
+    import lopec.runtime
+    from paper_1502_03504_b200.machine import machine_class
+    cls = machine_class()
+    assert issubclass(cls, lopec.runtime.Machine)
+    for name in ("_launch", "_halo_exchange", "gather", "run"):
+        assert getattr(cls, name) is not getattr(lopec.runtime.Machine, name), name
