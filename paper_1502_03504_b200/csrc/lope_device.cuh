@@ -387,6 +387,14 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   }
   auto produce = [&](lope_u32 limit) {
     while (p_L < limit && p_u < nunits) {
+#ifdef LOPE_STAGGER2
+      // experiment: delay the first load of odd-parity tiles' units
+      if (p_pl == 0 && ((pw.tx + pw.ty) & 1)) {
+        lope_u64 t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < (lope_u64)(LOPE_STAGGER2));
+      }
+#endif
       const lope_u32 slot = p_L % NS;
       if (p_L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((p_L / NS) - 1) & 1);
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);

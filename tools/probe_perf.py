@@ -24,6 +24,11 @@ k = R.CompiledKernel(kir, dt)
 fp = kir.footprints[kir.array_params[0]].dims
 a = R.HaloArray(shape, [n for n, _ in fp], [p for _, p in fp], dt)
 a.fill_hash(1)
+_gap = None
+if os.environ.get("GAP_GB"):
+    _gap = torch.empty(int(float(os.environ["GAP_GB"]) * (1 << 30)), dtype=torch.uint8, device="cuda")
+a.spare()
+print("in/out buffer addresses", hex(a.data.data_ptr()), hex(a.spare().data_ptr()), file=sys.stderr)
 R.halo_transfer(a)
 for _ in range(3):
     R.step(k, a)
