@@ -349,6 +349,13 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int zc = g.zchunk;
   const int nzc = (g.ext[2] + zc - 1) / zc;
   const int nunits = ntx * nty * nzc;     // < 2^31 (host checks)
+#ifdef LOPE_WALK_ZY
+  // experiment: walk x, then z-chunk, then y (y neighbours a whole x-z sweep apart)
+  constexpr bool ZY = true;
+#else
+  constexpr bool ZY = false;
+#endif
+  const int nmid = ZY ? nzc : nty;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -361,6 +368,11 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
     }
     lope_fence_init();
   }
+  // Programmatic dependent launch: let the next step's grid be scheduled now, and
+  // wait for the previous kernel's writes before the first global access (both are
+  // no-ops for a plain launch).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   // ---------------- TMA producer state (warp 0, lane 0) ----------------
@@ -376,12 +388,12 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int oz = g.lo[2] + g.r0[2] - FZN;
   const int pwarp = PW ? C::NCW : 0;     // the warp that issues TMA
   if (warp == pwarp && lane == 0) {
-    pw.init(blockIdx.x, gridDim.x, nty, ntx);
+    pw.init(blockIdx.x, gridDim.x, nmid, ntx);
     if (p_u < nunits) {
-      const int z0 = pw.zi * zc;
+      const int z0 = (ZY ? pw.ty : pw.zi) * zc;
       p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
       p_bx = g.box0 + pw.tx * C::BX;
-      p_by = oy + pw.ty * C::BY;
+      p_by = oy + (ZY ? pw.zi : pw.ty) * C::BY;
       p_z = oz + z0;
     }
   }
@@ -408,10 +420,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
         p_u += gridDim.x;
         pw.next();
         if (p_u < nunits) {
-          const int z0 = pw.zi * zc;
+          const int z0 = (ZY ? pw.ty : pw.zi) * zc;
           p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
           p_bx = g.box0 + pw.tx * C::BX;
-          p_by = oy + pw.ty * C::BY;
+          p_by = oy + (ZY ? pw.zi : pw.ty) * C::BY;
           p_z = oz + z0;
         }
       }
@@ -437,14 +449,14 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
 
   LopeUnitWalk w;
-  w.init(blockIdx.x, gridDim.x, nty, ntx);
+  w.init(blockIdx.x, gridDim.x, nmid, ntx);
   lope_u32 lbase = 0;
   T hist[FZN > 0 ? FZN : 1][RY][VX];
   for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
-    const int z0 = w.zi * zc;
+    const int z0 = (ZY ? w.ty : w.zi) * zc;
     const int nz = min(zc, g.ext[2] - z0);
     const int x = w.tx * C::BX + cx;
-    const int ybase = w.ty * C::BY + row0;
+    const int ybase = (ZY ? w.zi : w.ty) * C::BY + row0;
     const bool xok = x < g.ext[0];
     const int nrow = min(RY, g.ext[1] - ybase);
     // Periodic images (lope_step): x images are whole 64-byte atoms written by the
