@@ -274,6 +274,18 @@ struct Emitter {
           double fr = std::frexp(d.value, &e);
           if ((fr == 0.5 || fr == -0.5) && e > -100 && e < 100)
             return "A_::mul(" + ex(n.kids[0]) + ", T(" + hexlit(1.0 / d.value) + "))";
+          // any other constant: reciprocal + FMA correction (LopeAr::divc), with the
+          // correctly rounded reciprocal of the divisor as converted to each type
+          const float bf = (float)d.value;
+          const double yf = (double)(1.0f / bf);
+          const double yd = 1.0 / d.value;
+          const float abf = std::fabs(bf);
+          const double abd = std::fabs(d.value);
+          const bool okf = std::isfinite(bf) && abf >= 0x1p-16f && abf <= 0x1p+16f && std::isfinite(yf);
+          const bool okd = abd >= 0x1p-60 && abd <= 0x1p+60;
+          has_divc = true;
+          return "A_::template divc<FAST>(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ", " + hexlit(yf) + ", " +
+                 hexlit(yd) + ", " + (okf ? "true" : "false") + ", " + (okd ? "true" : "false") + ", slow)";
         }
         return "A_::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
       }
@@ -291,6 +303,7 @@ struct Emitter {
     return "T(0)";
   }
   std::set<std::string> assigned;   // locals assigned so far
+  bool has_divc = false;            // a constant division went through LopeAr::divc
 };
 
 }  // namespace
@@ -316,23 +329,30 @@ std::string emit_body(const Kir& k) {
   o << "  static __device__ __forceinline__ constexpr int stored(int q) { return ";
   for (size_t i = 0; i + 1 < k.stored.size(); ++i) o << "q == " << i << " ? " << k.stored[i] << " : ";
   o << k.stored.back() << "; }\n";
-  o << "  template <class T, class RD>\n";
-  o << "  static __device__ __forceinline__ void eval(const RD& rd, const T* __restrict__ sc, T* res) {\n";
-  o << "    typedef LopeAr<T> A_;\n";
-  o << "    (void)sc;\n";
-  for (size_t i = 0; i < k.locals.size(); ++i) o << "    T l" << i << " = T(0);\n";
-  for (int a : k.stored) o << "    T p" << a << " = T(0);\n";
+  // FAST evaluation (tiled kernel) keeps every point branch-free so the compiler can
+  // interleave the points' dependency chains; a constant division whose operand lies
+  // outside its fast range sets `slow` and the caller re-evaluates with FAST = false.
   Emitter E(k);
+  std::ostringstream b;
   for (const Stmt& st : k.body) {
     std::string rhs = E.ex(st.expr);
     if (st.is_array) {
-      o << "    p" << st.target << " = " << rhs << ";\n";
+      b << "    p" << st.target << " = " << rhs << ";\n";
       E.pending.insert(st.target);
     } else {
-      o << "    l" << st.target << " = " << rhs << ";\n";
+      b << "    l" << st.target << " = " << rhs << ";\n";
       E.assigned.insert(k.locals[st.target]);
     }
   }
+  o << "  static constexpr bool HAS_DIVC = " << (E.has_divc ? "true" : "false") << ";\n";
+  o << "  template <class T, bool FAST, class RD>\n";
+  o << "  static __device__ __forceinline__ void eval(const RD& rd, const T* __restrict__ sc, T* res, bool& slow) {\n";
+  o << "    typedef LopeAr<T> A_;\n";
+  o << "    (void)sc;\n";
+  o << "    (void)slow;\n";
+  for (size_t i = 0; i < k.locals.size(); ++i) o << "    T l" << i << " = T(0);\n";
+  for (int a : k.stored) o << "    T p" << a << " = T(0);\n";
+  o << b.str();
   for (size_t q = 0; q < k.stored.size(); ++q) o << "    res[" << q << "] = p" << k.stored[q] << ";\n";
   o << "  }\n};\n";
   return o.str();

@@ -39,6 +39,34 @@ template <> struct LopeAr<float> {
   static __device__ __forceinline__ float neg(float a) { return -a; }
   static __device__ __forceinline__ float abs_(float a) { return fabsf(a); }
   static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+  // x / b for a constant b with y = RN(1/b): q = RN(x*y) is within 1 ulp of x/b, the
+  // FMA residual r = x - q*b is exact, and RN(q + r*y) is the correctly rounded
+  // quotient (Markstein's theorem) -- same bits as the IEEE division, no divide
+  // sequence.  Outside the range where neither q nor r can underflow or overflow
+  // (and for 0, inf, NaN) it falls back to the IEEE division.  `ok` is false when
+  // the host found b unsuitable (zero, non-finite, |b| outside [2^-16, 2^16]).
+  template <bool FAST>
+  static __device__ __forceinline__ float divc(float x, float b, double yf, double, bool ok, bool, bool& slow) {
+    if (!ok) return __fdiv_rn(x, b);
+    const float y = (float)yf;
+    const float ax = fabsf(x);
+    if (FAST) {
+      // branch-free: 0 / inf / NaN give x*y (same bits as x/b); the tiny and huge
+      // ranges are flagged and recomputed by the caller with the exact path
+      const float q = __fmul_rn(x, y);
+      const float r = __fmaf_rn(-q, b, x);
+      const float m = __fmaf_rn(r, y, q);
+      const bool special = !(ax > 0.0f && ax <= 0x1.fffffep+127f);
+      slow |= !special && !(ax >= 0x1p-90f && ax <= 0x1p+90f);
+      return special ? q : m;
+    }
+    if (ax >= 0x1p-90f && ax <= 0x1p+90f) {
+      const float q = __fmul_rn(x, y);
+      const float r = __fmaf_rn(-q, b, x);
+      return __fmaf_rn(r, y, q);
+    }
+    return __fdiv_rn(x, b);
+  }
 };
 template <> struct LopeAr<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
@@ -47,6 +75,26 @@ template <> struct LopeAr<double> {
   static __device__ __forceinline__ double neg(double a) { return -a; }
   static __device__ __forceinline__ double abs_(double a) { return fabs(a); }
   static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+  // see LopeAr<float>::divc; the host requires |b| in [2^-60, 2^60]
+  template <bool FAST>
+  static __device__ __forceinline__ double divc(double x, double b, double, double yd, bool, bool ok, bool& slow) {
+    if (!ok) return __ddiv_rn(x, b);
+    const double ax = fabs(x);
+    if (FAST) {
+      const double q = __dmul_rn(x, yd);
+      const double r = __fma_rn(-q, b, x);
+      const double m = __fma_rn(r, yd, q);
+      const bool special = !(ax > 0.0 && ax <= 0x1.fffffffffffffp+1023);
+      slow |= !special && !(ax >= 0x1p-900 && ax <= 0x1p+900);
+      return special ? q : m;
+    }
+    if (ax >= 0x1p-900 && ax <= 0x1p+900) {
+      const double q = __dmul_rn(x, yd);
+      const double r = __fma_rn(-q, b, x);
+      return __fma_rn(r, yd, q);
+    }
+    return __ddiv_rn(x, b);
+  }
 };
 // numpy.minimum / numpy.maximum: NaN in either operand propagates; ties return the second.
 template <class T> __device__ __forceinline__ T lope_min(T a, T b) { return (a != a || a < b) ? a : b; }
@@ -151,7 +199,8 @@ __device__ __forceinline__ void lope_generic_impl(const LopeArr<T>* arrs, const 
       for (int q = 0; q < Body::NARR; ++q)
         rd.offs[q] = arrs[q].org + i + (lope_i64)j * arrs[q].s1 + (lope_i64)k * arrs[q].s2;
       T res[Body::NSTORE > 0 ? Body::NSTORE : 1];
-      Body::template eval<T>(rd, sc.v, res);
+      bool slow = false;
+      Body::template eval<T, false>(rd, sc.v, res, slow);
 #pragma unroll
       for (int q = 0; q < Body::NSTORE; ++q) {
         const int A = Body::stored(q);
@@ -278,6 +327,20 @@ struct LopeWinReader {
   __device__ __forceinline__ T at() const {
     if (ZHIST && DZ < 0) return hist[((-DZ - 1) * RY + r) * VX + v];
     return win[((DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0)];
+  }
+};
+
+// Reads the staged planes in shared memory directly (the exact re-evaluation of a
+// plane whose fast evaluation flagged a slow-range division).
+template <class T, int BOXX, int NZW, int FZN, int FN0, int FN1, int RY, int VX, bool ZHIST>
+struct LopeSmemReader {
+  const T* const* sp;  // [NZW] this lane's origin in each staged plane
+  const T* hist;
+  int r, v;
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ T at() const {
+    if (ZHIST && DZ < 0) return hist[((-DZ - 1) * RY + r) * VX + v];
+    return sp[DZ + FZN][(r + DY + FN1) * BOXX + v + DX];
   }
 };
 
@@ -523,6 +586,8 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       // outputs has all its inputs (short live ranges: no spills at 16 warps) ----
       T win[NZW][NR][NXW];
       T vals[RY][VX];
+      bool slow = false;
+      constexpr bool FAST = Body::HAS_DIVC;    // branch-free points, exact redo below
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
 #pragma unroll
@@ -548,10 +613,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
             rd.r = r;
             rd.v = v;
             T res[1];
-            Body::template eval<T>(rd, sc.v, res);
+            Body::template eval<T, FAST>(rd, sc.v, res, slow);
             vals[r][v] = res[0];
           }
-          if (ZHIST) {
+          if (ZHIST && !FAST) {
             // row r of the history only feeds row r: shift it now
 #pragma unroll
             for (int d = FZN - 1; d > 0; --d)
@@ -559,6 +624,40 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
               for (int e = 0; e < VX; ++e) hist[d][r][e] = hist[d - 1][r][e];
 #pragma unroll
             for (int e = 0; e < VX; ++e) hist[0][r][e] = win[FZN][Body::FN1 + r][Body::FN0 + e];
+          }
+        }
+      }
+      if (FAST) {
+        if (slow) {
+          // a division operand fell outside the fast range: redo this lane's points
+          // with the exact (branching) evaluation, straight from shared memory
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+              LopeSmemReader<T, C::BOXX, NZW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+              rd.sp = sp;
+              rd.hist = &hist[0][0][0];
+              rd.r = r;
+              rd.v = v;
+              T res[1];
+              bool dummy = false;
+              Body::template eval<T, false>(rd, sc.v, res, dummy);
+              vals[r][v] = res[0];
+            }
+          }
+        }
+        if (ZHIST) {
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+#pragma unroll
+            for (int d = FZN - 1; d > 0; --d)
+#pragma unroll
+              for (int e = 0; e < VX; ++e) hist[d][r][e] = hist[d - 1][r][e];
+            const V cv = *reinterpret_cast<const V*>(sp[FZN] + (Body::FN1 + r) * C::BOXX);
+            const T* ce = reinterpret_cast<const T*>(&cv);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) hist[0][r][e] = ce[e];
           }
         }
       }

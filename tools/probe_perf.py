@@ -18,6 +18,13 @@ elif name == "copy2dh":
 elif name == "copy3dz":
     from paper_1502_03504_b200.ir import KernelBuilder
     kb = KernelBuilder("copy3dz", 3); u = kb.array("u"); kb.store(u, u[0, 0, 0] + 0 * (u[0, 0, 1] + u[0, 0, -1])); kir = kb.build()
+elif name in ("box5x5m", "box5x5s"):
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder(name, 2); u = kb.array("u"); acc = None
+    for j in range(-2, 3):
+        for i in range(-2, 3):
+            acc = u[i, j] if acc is None else acc + u[i, j]
+    kb.store(u, acc * 0.04 if name == "box5x5m" else acc); kir = kb.build()
 else:
     kir = stencils.by_name(name)
 k = R.CompiledKernel(kir, dt)
