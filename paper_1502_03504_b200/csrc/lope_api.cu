@@ -13,11 +13,13 @@
 #include <nvrtc.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -276,7 +278,8 @@ struct DevMod {
 
 // host mirrors of the device parameter structs (lope_device.cuh)
 template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
-template <class T> struct HScal { T v[16]; };
+#define LOPE_HOST_MAX_SCAL 16   // == LOPE_MAX_SCAL in lope_device.cuh
+template <class T> struct HScal { T v[LOPE_HOST_MAX_SCAL]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
   int wrap, zchunk, xshift, box0, p1;
@@ -530,6 +533,18 @@ HScal<T> make_scal(const lope::Kir& k, const double* rs, const int64_t* is) {
   for (size_t i = 0; i < k.scalars.size(); ++i) {
     if (k.scalar_is_int[i]) s.v[i] = is ? (T)is[i] : (T)0;
     else s.v[i] = rs ? (T)rs[i] : (T)0;
+  }
+  // reciprocals for LopeAr::divs (scalar divisors): RN(1/b) in T when |b| lies in the
+  // range where the FMA-corrected quotient is exact, NaN (-> exact division) otherwise
+  const size_t n = k.scalars.size();
+  if (2 * n <= (size_t)LOPE_HOST_MAX_SCAL) {
+    const double lo = sizeof(T) == 4 ? 0x1p-16 : 0x1p-60, hi = sizeof(T) == 4 ? 0x1p+16 : 0x1p+60;
+    for (size_t i = 0; i < n; ++i) {
+      const T b = s.v[i];
+      const double ab = std::fabs((double)b);
+      s.v[n + i] = (std::isfinite((double)b) && ab >= lo && ab <= hi) ? (T)(T(1) / b)
+                                                                       : std::numeric_limits<T>::quiet_NaN();
+    }
   }
   return s;
 }

@@ -287,6 +287,13 @@ struct Emitter {
           return "A_::template divc<FAST>(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ", " + hexlit(yf) + ", " +
                  hexlit(yd) + ", " + (okf ? "true" : "false") + ", " + (okd ? "true" : "false") + ", slow)";
         }
+        if (d.kind == Node::SCALAR && !loc_ix.count(d.name) && 2 * k.scalars.size() <= 16) {
+          // kernel scalar divisor: the host passes RN(1/b) (or NaN) after the scalars
+          has_divc = true;
+          const int i = scal_ix.at(d.name);
+          return "A_::template divs<FAST>(" + ex(n.kids[0]) + ", sc[" + std::to_string(i) + "], sc[" +
+                 std::to_string(k.scalars.size() + i) + "], slow)";
+        }
         return "A_::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
       }
       case Node::NEG: return "A_::neg(" + ex(n.kids[0]) + ")";

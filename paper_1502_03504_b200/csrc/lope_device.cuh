@@ -45,6 +45,26 @@ template <> struct LopeAr<float> {
   // sequence.  Outside the range where neither q nor r can underflow or overflow
   // (and for 0, inf, NaN) it falls back to the IEEE division.  `ok` is false when
   // the host found b unsuitable (zero, non-finite, |b| outside [2^-16, 2^16]).
+  // x / b for a kernel scalar b; y = RN(1/b) from the host, NaN when b is outside
+  // the exact range (the point is then flagged and redone with the IEEE division)
+  template <bool FAST>
+  static __device__ __forceinline__ float divs(float x, float b, float y, bool& slow) {
+    const float ax = fabsf(x);
+    if (FAST) {
+      const float q = __fmul_rn(x, y);
+      const float r = __fmaf_rn(-q, b, x);
+      const float m = __fmaf_rn(r, y, q);
+      const bool special = !(ax > 0.0f && ax <= 0x1.fffffep+127f);
+      slow |= (y != y) || (!special && !(ax >= 0x1p-90f && ax <= 0x1p+90f));
+      return special ? q : m;
+    }
+    if (y == y && ax >= 0x1p-90f && ax <= 0x1p+90f) {
+      const float q = __fmul_rn(x, y);
+      const float r = __fmaf_rn(-q, b, x);
+      return __fmaf_rn(r, y, q);
+    }
+    return __fdiv_rn(x, b);
+  }
   template <bool FAST>
   static __device__ __forceinline__ float divc(float x, float b, double yf, double, bool ok, bool, bool& slow) {
     if (!ok) return __fdiv_rn(x, b);
@@ -76,6 +96,24 @@ template <> struct LopeAr<double> {
   static __device__ __forceinline__ double abs_(double a) { return fabs(a); }
   static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
   // see LopeAr<float>::divc; the host requires |b| in [2^-60, 2^60]
+  template <bool FAST>
+  static __device__ __forceinline__ double divs(double x, double b, double y, bool& slow) {
+    const double ax = fabs(x);
+    if (FAST) {
+      const double q = __dmul_rn(x, y);
+      const double r = __fma_rn(-q, b, x);
+      const double m = __fma_rn(r, y, q);
+      const bool special = !(ax > 0.0 && ax <= 0x1.fffffffffffffp+1023);
+      slow |= (y != y) || (!special && !(ax >= 0x1p-900 && ax <= 0x1p+900));
+      return special ? q : m;
+    }
+    if (y == y && ax >= 0x1p-900 && ax <= 0x1p+900) {
+      const double q = __dmul_rn(x, y);
+      const double r = __fma_rn(-q, b, x);
+      return __fma_rn(r, y, q);
+    }
+    return __ddiv_rn(x, b);
+  }
   template <bool FAST>
   static __device__ __forceinline__ double divc(double x, double b, double, double yd, bool, bool ok, bool& slow) {
     if (!ok) return __ddiv_rn(x, b);

@@ -150,3 +150,30 @@ def test_box5x5_wide_range_matches_oracle(dtype):
     with np.errstate(all="ignore"):
         want = O.periodic_apply(field, kir, dtype=npd)
     assert O.equal_bits(arr.get_interior(), want), O.first_mismatch(arr.get_interior(), want)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_scalar_divisor_matches_ieee(dtype):
+    """x / s for a kernel scalar s (host-side reciprocal, NaN for unsafe s)."""
+    from paper_1502_03504_b200 import runtime as R
+    from paper_1502_03504_b200.ir import KernelBuilder
+    kb = KernelBuilder("divs", 2)
+    u = kb.array("u")
+    s = kb.scalar("s")
+    kb.store(u, (u[0, 0] + u[1, 0]) / s)
+    kir = kb.build()
+    name = "float64" if dtype == np.float64 else "float32"
+    k = R.CompiledKernel(kir, name)
+    rng = np.random.default_rng(3)
+    shape = (1024, 512)
+    x = _random_bits(rng, shape[0] * shape[1], dtype).reshape(shape, order="F")
+    for sv in (25.0, 0.1, -3.0, 7.0, 0.0, 1e-30, 3e20, float("inf"), float("nan")):
+        arr = R.HaloArray(shape, [0, 0], [1, 0], name)
+        arr.set_interior(x)
+        R.halo_transfer(arr)
+        R.launch(k, [arr], scalars={"s": sv})
+        with np.errstate(all="ignore"):
+            xr = np.roll(x, -1, axis=0)
+            want = ((x + xr) / dtype(sv)).astype(dtype)
+        got = arr.get_interior()
+        assert equal_bits(got, want), f"s={sv}: {np.argwhere(~((got == want) | (np.isnan(got) & np.isnan(want))))[:3]}"
