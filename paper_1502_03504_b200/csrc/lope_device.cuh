@@ -391,7 +391,11 @@ struct LopeTiledCfg {
   static constexpr int BOXX = PADX + BX + ((Body::FP0 + VX - 1) / VX) * VX;
   static constexpr int BOXY = BY + Body::FN1 + Body::FP1;
   static constexpr int NZW = Body::FN2 + Body::FP2 + 1;
+#ifdef LOPE_NO_ZHIST
+  static constexpr bool ZHIST = false;   // experiment: all z planes from the ring
+#else
   static constexpr bool ZHIST = Body::ZSTAR && Body::FN2 > 0;
+#endif
   static constexpr int HOLD = ZHIST ? Body::FP2 + 1 : NZW;     // slots one plane iteration holds
   static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
   static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
