@@ -330,6 +330,8 @@ def run_gpu_arm(args, wl):
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
                 "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
                 "kernel_ms": round(kernel_ms, 4),
+                "step_ms_min_med_max": [round(min(per_step), 4), round(sorted(per_step)[len(per_step) // 2], 4),
+                                        round(max(per_step), 4)],
                 "pct_of_8TBs": round(100 * alg_bytes / (kernel_ms / 1e3) / 8e12, 1)}
 
     # e2e through the public API, host buffers, H2D + E2E_ITERS iterations + D2H timed

@@ -133,6 +133,16 @@ int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const i
 /* Fill the interior with the synthetic U(-1,1) field: value of global cell
  * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
  * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */
+/* Box <-> contiguous device buffer (column-major within the box, dim 1 fastest):
+ * `extent` cells at padded coordinates `lo`.  Faces of a decomposed dimension other
+ * than the slowest are strided; they are packed into a buffer, sent between GPUs
+ * and unpacked into the neighbour's halo (the slabs of runtime.py:664-697 for an
+ * MP x NP image grid, grid.py:22-61).  E108 if the box leaves the padded block. */
+int lope_box_pack(const lope_layout* layout, const void* blk, const int64_t* lo, const int64_t* extent,
+                  void* buf, void* stream);
+int lope_box_unpack(const lope_layout* layout, void* blk, const int64_t* lo, const int64_t* extent,
+                    const void* buf, void* stream);
+
 int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const int64_t* global_extent,
                    const int64_t* global_origin, void* stream);
 

@@ -232,6 +232,27 @@ __global__ void __launch_bounds__(256) lope_k_copy_box(T* __restrict__ dst, cons
   }
 }
 
+// Box <-> contiguous buffer (column-major within the box): the strided faces of a
+// decomposed non-slowest dim travel between GPUs through such buffers.
+template <class T, bool PACK>
+__global__ void __launch_bounds__(256) lope_k_box_xfer(T* __restrict__ blk, T* __restrict__ buf, DevLayout L,
+                                                       long long b0, long long b1, long long b2, long long e0,
+                                                       long long e1, long long e2) {
+  const long long nrows = e1 * e2;
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < nrows; r += nw) {
+    const long long j = r % e1, k = r / e1;
+    T* brow = blk + L.B + b0 + (b1 + j) * L.S1 + (b2 + k) * L.S2;
+    T* crow = buf + r * e0;
+    for (long long x = lane; x < e0; x += 32) {
+      if (PACK) crow[x] = brow[x];
+      else brow[x] = crow[x];
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned long long lope_splitmix64(unsigned long long x) {
   unsigned long long z = x + 0x9E3779B97F4A7C15ULL;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -339,11 +360,11 @@ int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
 }
 
 TileCfg pick_tile(const lope::Kir& k, int dtype) {
-  // One CTA per SM: 16 compute warps stacked in y plus one TMA producer warp.  Lanes
-  // hold 16-byte vectors (4 fp32 / 2 fp64), so a tile is one warp (128 fp32 / 64 fp64
-  // columns) wide and the TMA box stays within 256 elements.  Calibrated on B200
-  // (tools/probe_perf.py): 3-D fp32 best at 4 rows/lane (64-row tiles, 6 x 36 KB ring),
-  // 2-D at 2 rows/lane (32-row tiles, 12 x 18.5 KB ring).
+  // One CTA per SM: 16 compute warps stacked in y (plus a TMA producer warp for 2-D).
+  // Lanes hold 16-byte vectors (4 fp32 / 2 fp64), so a tile is one warp (128 fp32 / 64
+  // fp64 columns) wide and the TMA box stays within 256 elements.  Calibrated on B200
+  // (tools/probe_perf.py): 2 rows/lane (32-row tiles, 18.5 KB stages); 2-D fills the
+  // ring (12 stages), 3-D runs best with 8 (lap3d7 1024^3: 1.62 ms vs 1.67 ms at 12).
   TileCfg c;
   const int nzw = k.fn[0][2] + k.fp[0][2] + 1;
   bool zstar = k.rank == 3;
@@ -379,6 +400,7 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
     if (dtype == LOPE_F32)
       while (c.ry > 1 && window(c.ry) > 64) c.ry /= 2;
   }
+  if (k.rank == 3 && dtype == LOPE_F32) c.ns = 8;
   if (const char* e = std::getenv("LOPE_TILE")) {
     int a, b, cc, d;
     if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &cc, &d) == 4) {
@@ -1095,6 +1117,55 @@ int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const i
   CUDA_TRY(cudaGetLastError());
   g_launches++;
   return 0;
+}
+
+namespace {
+int box_xfer(const lope_layout* layout, void* blk, void* buf, const int64_t* lo, const int64_t* extent,
+             void* stream, bool pack) {
+  if (int e = check_layout(layout)) return e;
+  if (!blk || !buf || !lo || !extent) return fail(202, "null argument");
+  for (int d = 0; d < 3; ++d) {
+    if (extent[d] < 0 || lo[d] < 0 || lo[d] + extent[d] > layout->padded[d])
+      return fail(108, "box outside the padded block in dim %d", d + 1);
+    if (extent[d] == 0) return 0;
+  }
+  DevLayout d = dev_layout(layout);
+  cudaStream_t st = (cudaStream_t)stream;
+  long long rows = extent[1] * extent[2];
+  long long blocks = (rows * 32 + 255) / 256;
+  long long cap = (long long)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const int nb = (int)blocks;
+  if (layout->dtype == LOPE_F32) {
+    if (pack)
+      lope_k_box_xfer<float, true><<<nb, 256, 0, st>>>((float*)blk, (float*)buf, d, lo[0], lo[1], lo[2],
+                                                        extent[0], extent[1], extent[2]);
+    else
+      lope_k_box_xfer<float, false><<<nb, 256, 0, st>>>((float*)blk, (float*)buf, d, lo[0], lo[1], lo[2],
+                                                         extent[0], extent[1], extent[2]);
+  } else {
+    if (pack)
+      lope_k_box_xfer<double, true><<<nb, 256, 0, st>>>((double*)blk, (double*)buf, d, lo[0], lo[1], lo[2],
+                                                         extent[0], extent[1], extent[2]);
+    else
+      lope_k_box_xfer<double, false><<<nb, 256, 0, st>>>((double*)blk, (double*)buf, d, lo[0], lo[1], lo[2],
+                                                          extent[0], extent[1], extent[2]);
+  }
+  CUDA_TRY(cudaGetLastError());
+  g_launches++;
+  return 0;
+}
+}  // namespace
+
+int lope_box_pack(const lope_layout* layout, const void* blk, const int64_t* lo, const int64_t* extent,
+                  void* buf, void* stream) {
+  return box_xfer(layout, const_cast<void*>(blk), buf, lo, extent, stream, true);
+}
+
+int lope_box_unpack(const lope_layout* layout, void* blk, const int64_t* lo, const int64_t* extent,
+                    const void* buf, void* stream) {
+  return box_xfer(layout, blk, const_cast<void*>(buf), lo, extent, stream, false);
 }
 
 int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const int64_t* gext,

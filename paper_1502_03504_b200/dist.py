@@ -338,3 +338,308 @@ def run_pinned(kernel, local_shape, lo, hi, dtype, host_in, host_out, steps, gro
     SlabStepper(kernel, arr, scalars).iterate(steps)
     arr.block.download(host_out.data_ptr())
     torch.cuda.current_stream().synchronize()
+
+
+# ---------------------------------------------------------------------------
+# General process grids: MP x NP for 2-D (the reference's grid.py), P0 x P1 x P2 for 3-D
+
+
+class CartGrid:
+    """Cartesian decomposition of ``global_shape`` over ``prod(splits)`` images.
+
+    ``splits[d]`` blocks along array dim d+1.  Ranks are numbered with the slowest
+    array dim varying fastest, which for 2-D is exactly the reference's column-major
+    image order (``grid.py:1-13``: ``prow = (k-1) mod MP`` indexes dim 2, ``pcol``
+    dim 1), so ``CartGrid.from_images(shape, images, grid_rows)`` places every block
+    where ``Machine._setup_extents`` (runtime.py:135-189) does.
+    """
+
+    def __init__(self, global_shape: Sequence[int], splits: Sequence[int], lo: Sequence[int], hi: Sequence[int]):
+        self.global_shape = tuple(int(m) for m in global_shape)
+        self.splits = tuple(int(s) for s in splits)
+        if len(self.splits) != len(self.global_shape):
+            raise RuntimeFault(GRID_FACTOR, f"{len(self.splits)} grid factors for a rank-"
+                                            f"{len(self.global_shape)} array")
+        if any(s < 1 for s in self.splits):
+            raise RuntimeFault(GRID_FACTOR, f"grid factors {self.splits} must be at least 1")
+        self.nranks = int(np.prod(self.splits))
+        local = []
+        for d, (n, s) in enumerate(zip(self.global_shape, self.splits)):
+            if n % s:
+                # runtime.py:171-188 (E201)
+                raise RuntimeFault(GRID_FACTOR, f"global extent {n} (dim {d + 1}) is not divisible by "
+                                                f"the {s} image(s) along it")
+            m = n // s
+            if s > 1 and (lo[d] > m or hi[d] > m):
+                raise RuntimeFault(ALLOC_SHAPE, f"halo widths ({lo[d]},{hi[d]}) exceed the per-image extent "
+                                                f"{m} of decomposed dim {d + 1}")
+            local.append(m)
+        self.local_shape = tuple(local)
+        self.lo = tuple(int(w) for w in lo)
+        self.hi = tuple(int(w) for w in hi)
+
+    @classmethod
+    def from_images(cls, global_shape, images: int, grid_rows: int, lo, hi):
+        """The reference's ``RunConfig(images=P, grid_rows=MP)`` (grid.py:50-61)."""
+        if images < 1 or grid_rows < 1 or images % grid_rows:
+            raise RuntimeFault(GRID_FACTOR, f"cannot factor {images} image(s) into {grid_rows} grid row(s)")
+        rank = len(global_shape)
+        if rank == 1:
+            if grid_rows != 1:
+                raise RuntimeFault(GRID_FACTOR, "rank-1 arrays need grid_rows = 1")
+            return cls(global_shape, (images,), lo, hi)
+        if rank != 2:
+            raise RuntimeFault(GRID_FACTOR, "the reference's image grid decomposes rank <= 2 arrays")
+        return cls(global_shape, (images // grid_rows, grid_rows), lo, hi)
+
+    def coords(self, rank: int):
+        c = [0] * len(self.splits)
+        r = int(rank)
+        for d in reversed(range(len(self.splits))):
+            c[d] = r % self.splits[d]
+            r //= self.splits[d]
+        return tuple(c)
+
+    def rank_at(self, coords) -> int:
+        r = 0
+        for d in range(len(self.splits)):
+            r = r * self.splits[d] + (int(coords[d]) % self.splits[d])
+        return r
+
+    def neighbour(self, rank: int, d: int, delta: int) -> int:
+        c = list(self.coords(rank))
+        c[d] += delta
+        return self.rank_at(c)
+
+    def origin(self, rank: int):
+        return tuple(c * m for c, m in zip(self.coords(rank), self.local_shape))
+
+    @property
+    def local_mask(self) -> int:
+        """Dims whose neighbour is the image itself (wrapped on the GPU)."""
+        return sum(1 << d for d, s in enumerate(self.splits) if s == 1)
+
+
+def face_boxes(layout, d: int):
+    """The four slabs of ``_halo_exchange`` along dim d (runtime.py:659-667), as
+    (lo, extent) boxes in padded coordinates spanning the full padded block in the
+    other dims: low_halo, high_halo, first `hi` interior planes, last `lo` planes."""
+    L = layout
+    r = int(L.rank)
+    padded = [int(L.padded[i]) if i < r else 1 for i in range(3)]
+    lo_d, hi_d, m_d = int(L.lo[d]), int(L.hi[d]), int(L.interior[d])
+
+    def box(start, width):
+        b = [0, 0, 0]
+        e = list(padded)
+        b[d] = start
+        e[d] = width
+        return tuple(b), tuple(e)
+
+    return {"low_halo": box(0, lo_d), "high_halo": box(lo_d + m_d, hi_d),
+            "first": box(lo_d, hi_d), "last": box(m_d, lo_d)}
+
+
+class DevicePacker:
+    """Face staging on the GPU through the C ABI (lope_box_pack / lope_box_unpack)."""
+
+    @staticmethod
+    def alloc(flat, box):
+        import torch
+        return torch.empty(int(np.prod(box[1])), dtype=flat.dtype, device=flat.device)
+
+    def pack(self, flat, layout, box, stream=None):
+        (b, e) = box
+        buf = self.alloc(flat, box)
+        _lib.check(_lib.lib().lope_box_pack(ctypes.byref(layout), ctypes.c_void_p(flat.data_ptr()),
+                                            (ctypes.c_int64 * 3)(*b), (ctypes.c_int64 * 3)(*e),
+                                            ctypes.c_void_p(buf.data_ptr()), _stream_ptr(stream)),
+                   "lope_box_pack")
+        return buf
+
+    def unpack(self, flat, layout, box, buf, stream=None):
+        (b, e) = box
+        _lib.check(_lib.lib().lope_box_unpack(ctypes.byref(layout), ctypes.c_void_p(flat.data_ptr()),
+                                              (ctypes.c_int64 * 3)(*b), (ctypes.c_int64 * 3)(*e),
+                                              ctypes.c_void_p(buf.data_ptr()), _stream_ptr(stream)),
+                   "lope_box_unpack")
+
+    def local_wrap(self, flat, layout, d: int, stream=None):
+        _lib.check(_lib.lib().lope_halo_fill(ctypes.byref(layout), ctypes.c_void_p(flat.data_ptr()), 1 << d,
+                                             _stream_ptr(stream)), "lope_halo_fill")
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(int(s.cuda_stream))
+
+
+class GridExchanger:
+    """``_halo_exchange`` (runtime.py:643-711) between the images of a ``CartGrid``:
+    dims in ascending order, each finished everywhere before the next (so corners
+    arrive through the full-extent slabs); a dim split over one image wraps locally,
+    otherwise its two faces travel to the cyclic neighbours over ``torch.distributed``
+    point-to-point (NCCL between GPUs), packed when they are strided."""
+
+    def __init__(self, grid: CartGrid, group=None, packer=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.grid = grid
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.packer = packer or DevicePacker()
+
+    def _g(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def exchange(self, flat, layout, stream=None, dims=None) -> None:
+        dist = self.dist
+        rank = int(layout.rank)
+        for d in range(rank):
+            if dims is not None and not (dims >> d) & 1:
+                continue
+            lo_d, hi_d = int(layout.lo[d]), int(layout.hi[d])
+            if lo_d == 0 and hi_d == 0:
+                continue
+            if self.grid.splits[d] == 1:
+                self.packer.local_wrap(flat, layout, d, stream)
+                continue
+            fb = face_boxes(layout, d)
+            prev = self._g(self.grid.neighbour(self.rank, d, -1))
+            nxt = self._g(self.grid.neighbour(self.rank, d, +1))
+            send_next = self.packer.pack(flat, layout, fb["last"], stream) if lo_d else None
+            send_prev = self.packer.pack(flat, layout, fb["first"], stream) if hi_d else None
+            recv_low = self.packer.alloc(flat, fb["low_halo"]) if lo_d else None
+            recv_high = self.packer.alloc(flat, fb["high_halo"]) if hi_d else None
+            ops = []
+            # same order on every rank: NCCL pairs the two directions correctly even when
+            # prev == next (two images along d)
+            if send_next is not None:
+                ops.append(dist.P2POp(dist.isend, send_next, nxt, self.group, TAG_LOW))
+            if send_prev is not None:
+                ops.append(dist.P2POp(dist.isend, send_prev, prev, self.group, TAG_HIGH))
+            if recv_low is not None:
+                ops.append(dist.P2POp(dist.irecv, recv_low, prev, self.group, TAG_LOW))
+            if recv_high is not None:
+                ops.append(dist.P2POp(dist.irecv, recv_high, nxt, self.group, TAG_HIGH))
+            import torch
+            ctx = torch.cuda.stream(stream) if (stream is not None and flat.is_cuda) else _null()
+            with ctx:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            if recv_low is not None:
+                self.packer.unpack(flat, layout, fb["low_halo"], recv_low, stream)
+            if recv_high is not None:
+                self.packer.unpack(flat, layout, fb["high_halo"], recv_high, stream)
+
+
+class GridArray:
+    """This rank's block of an array decomposed over a ``CartGrid``."""
+
+    def __init__(self, grid: CartGrid, dtype="float32", group=None, exchanger=None):
+        from .runtime import HaloArray
+        self.grid = grid
+        self.block = HaloArray(grid.local_shape, grid.lo, grid.hi, dtype)
+        self.exchanger = exchanger or GridExchanger(grid, group)
+        self.rank = self.exchanger.rank
+
+    def halo_transfer(self, stream=None) -> None:
+        self.exchanger.exchange(self.block.data, self.block.layout, stream)
+
+
+class GridStepper:
+    """Fused step on a grid block: kernel (local dims' images refreshed in its
+    epilogue), then the decomposed dims' faces, ascending."""
+
+    def __init__(self, kernel, arr: GridArray, scalars=None):
+        self.kernel = kernel
+        self.arr = arr
+        self.scalars = scalars
+        self._remote = sum(1 << d for d, s in enumerate(arr.grid.splits) if s > 1)
+
+    def step(self) -> None:
+        from .runtime import step
+        blk = self.arr.block
+        step(self.kernel, blk, self.scalars, wrap_mask=self.arr.grid.local_mask)
+        if self._remote:
+            self.arr.exchanger.exchange(blk.data, blk.layout, dims=self._remote)
+
+    def iterate(self, steps: int) -> None:
+        from .runtime import launch
+        if steps <= 0:
+            return
+        self.arr.halo_transfer()
+        for _ in range(steps - 1):
+            self.step()
+        launch(self.kernel, [self.arr.block], None, self.scalars)
+
+
+class MultiGrid:
+    """All images of a ``CartGrid`` on one GPU, faces moved with ``lope_copy_box``
+    between the blocks in the exchange order: the grid pipeline checked against a
+    single-block run without needing more GPUs."""
+
+    def __init__(self, kernel, grid: CartGrid, dtype, scalars=None):
+        from .runtime import HaloArray
+        self.grid = grid
+        self.kernel = kernel
+        self.scalars = scalars
+        self.blocks = [HaloArray(grid.local_shape, grid.lo, grid.hi, dtype) for _ in range(grid.nranks)]
+
+    def set_global(self, field: np.ndarray) -> None:
+        for r, b in enumerate(self.blocks):
+            o = self.grid.origin(r)
+            sl = tuple(slice(o[d], o[d] + self.grid.local_shape[d]) for d in range(field.ndim))
+            b.set_interior(np.ascontiguousarray(field[sl]))
+
+    def get_global(self) -> np.ndarray:
+        out = np.empty(self.grid.global_shape, dtype=self.blocks[0].get_interior().dtype)
+        for r, b in enumerate(self.blocks):
+            o = self.grid.origin(r)
+            sl = tuple(slice(o[d], o[d] + self.grid.local_shape[d]) for d in range(out.ndim))
+            out[sl] = b.get_interior()
+        return out
+
+    def exchange(self, dims=None) -> None:
+        from .runtime import halo_transfer
+        L = self.blocks[0].layout
+        for d in range(int(L.rank)):
+            if dims is not None and not (dims >> d) & 1:
+                continue
+            if int(L.lo[d]) == 0 and int(L.hi[d]) == 0:
+                continue
+            if self.grid.splits[d] == 1:
+                for b in self.blocks:
+                    halo_transfer(b, dims_mask=1 << d)
+                continue
+            fb = face_boxes(L, d)
+            for r, b in enumerate(self.blocks):
+                prev = self.blocks[self.grid.neighbour(r, d, -1)]
+                nxt = self.blocks[self.grid.neighbour(r, d, +1)]
+                for dst_box, src_blk, src_box in ((fb["low_halo"], prev, fb["last"]),
+                                                  (fb["high_halo"], nxt, fb["first"])):
+                    if dst_box[1][d] == 0:
+                        continue
+                    _lib.check(_lib.lib().lope_copy_box(
+                        ctypes.byref(L), ctypes.c_void_p(b.data.data_ptr()), ctypes.c_void_p(src_blk.data.data_ptr()),
+                        (ctypes.c_int64 * 3)(*dst_box[0]), (ctypes.c_int64 * 3)(*src_box[0]),
+                        (ctypes.c_int64 * 3)(*dst_box[1]), _stream_ptr(None)), "lope_copy_box")
+
+    def step(self) -> None:
+        from .runtime import step
+        for b in self.blocks:
+            step(self.kernel, b, self.scalars, wrap_mask=self.grid.local_mask)
+        remote = sum(1 << d for d, s in enumerate(self.grid.splits) if s > 1)
+        if remote:
+            self.exchange(dims=remote)
+
+    def iterate(self, steps: int) -> None:
+        from .runtime import launch
+        if steps <= 0:
+            return
+        self.exchange()
+        for _ in range(steps - 1):
+            self.step()
+        for b in self.blocks:
+            launch(self.kernel, [b], None, self.scalars)

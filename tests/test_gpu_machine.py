@@ -77,3 +77,27 @@ def test_gpu_machine_fp32_matches_restatement():
     for _ in range(3):
         want = O.periodic_apply(want, kir, None, np.float32)
     assert O.equal_bits(m.gather().astype(np.float32), want)
+
+
+def test_cli_run_matches_reference_output(tmp_path, capsys):
+    """``python -m paper_1502_03504_b200.cli run`` prints exactly what ``lopec run``
+    prints for the same program (the reference Machine's gathered field, %.17g)."""
+    import io
+    from lopec.arrayio import write_array
+    from paper_1502_03504_b200 import cli
+    for case in CASES:
+        src = tmp_path / f"{case['tag']}.lope"
+        src.write_text(case["text"])
+        fin = tmp_path / f"{case['tag']}.in"
+        buf = io.StringIO()
+        write_array(buf, ARR[case["tag"] + "_in"])
+        fin.write_text(buf.getvalue())
+        out = tmp_path / f"{case['tag']}.out"
+        rc = cli.main(["run", str(src), "--images", str(case["images"]), "--grid-rows",
+                       str(case["grid_rows"]), "--devices", str(case["devices"]), "--steps", str(case["steps"]),
+                       "--input", str(fin),
+                       "-o", str(out)])
+        assert rc == 0
+        want = io.StringIO()
+        write_array(want, ARR[case["tag"] + "_out"])
+        assert out.read_text() == want.getvalue(), case["tag"]
