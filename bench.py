@@ -268,6 +268,15 @@ def run_gpu_arm(args, wl):
         def do_step():
             R.step(kern, arr)
 
+    # plan selection (runtime.PlanTuner): real steps under each candidate plan, part
+    # of setup like compilation; the timed steps run the chosen plan
+    tune_steps = 0
+    if ws > 1:
+        tune_steps = stepper.tune()
+    else:
+        while kern.tuner(arr, (1 << arr.rank) - 1) is not None:
+            do_step()
+            tune_steps += 1
     for _ in range(args.warmup):
         do_step()
     torch.cuda.synchronize()
@@ -359,6 +368,7 @@ def run_gpu_arm(args, wl):
                        "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
                              else "L2-resident working set (config 1); HBM fraction informational",
                        "hbm_gbs_alg": round(alg_bytes * ws / (ms_per_step / 1e3) / 1e9 / ws, 1)},
+            "plan": {"chosen": json.loads(kern.describe()).get("plans"), "tuning_steps": tune_steps},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -80,6 +80,8 @@ def precompile_kernels() -> list:
         text = serialize(stencils.by_name(name))
         for dt in dtypes:
             k = _lib.compile_kernel(text, dt)
+            if name in ("lap3d7", "ninept2d", "box5x5", "heat2d"):
+                _lib.check(_lib.lib().lope_kernel_prepare(k), "lope_kernel_prepare")   # tuning variants
             _lib.destroy_kernel(k)
             done.append(f"{name}:{dt}")
     return done

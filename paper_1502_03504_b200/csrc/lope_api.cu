@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -308,15 +309,31 @@ struct HGeom {
 
 }  // namespace
 
+// One compiled specialisation of a kernel (tile shape, ring depth, producer warp).
+struct LopeVariant {
+  TileCfg tile;
+  bool tiled_ok = false;
+  std::string source;
+  std::vector<char> cubin;
+  std::map<int, DevMod> mods;   // per device
+};
+
+// The execution plan for one geometry (lope_plan_set): the variant and the z-chunk.
+struct LopePlan {
+  int variant = 0;
+  int zchunk = 0;
+  double ms = 0.0;
+};
+
 struct lope_kernel {
   lope::Kir ir;
   int dtype = LOPE_F32;
-  bool tiled_ok = false;
-  TileCfg tile;
-  std::string source;
-  std::vector<char> cubin;
-  std::map<int, DevMod> mods;
+  std::vector<LopeVariant> variants;        // [0] = the default pick_tile() variant
+  std::map<std::string, LopePlan> plans;    // geometry key -> tuned plan
   std::string describe_path;
+  // the default variant's fields, kept for describe/source
+  const TileCfg& tile() const { return variants[0].tile; }
+  bool tiled_ok() const { return variants[0].tiled_ok; }
 };
 
 namespace {
@@ -415,7 +432,7 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
   return c;
 }
 
-std::string build_source(lope_kernel* K) {
+std::string build_source(const lope_kernel* K, const LopeVariant& V) {
   const lope::Kir& k = K->ir;
   std::ostringstream s;
   s << kDeviceSrc << "\n";
@@ -426,8 +443,8 @@ std::string build_source(lope_kernel* K) {
   s << "extern \"C\" __global__ void __launch_bounds__(128) lope_generic("
        "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
        "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n}\n";
-  if (K->tiled_ok) {
-    const TileCfg& c = K->tile;
+  if (V.tiled_ok) {
+    const TileCfg& c = V.tile;
     s << "typedef LopeTiledCfg<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
       << ", " << c.pw << "> LopeCfg;\n";
     s << "extern \"C\" __constant__ int lope_tiled_info[4] = {LopeCfg::SMEM_BYTES, LopeCfg::THREADS, "
@@ -499,11 +516,12 @@ int nvrtc_compile(const std::string& src, const std::string& name, std::vector<c
   return 0;
 }
 
-int get_mod(lope_kernel* K, DevMod** out) {
+int get_mod(lope_kernel* K, int vi, DevMod** out) {
+  LopeVariant& V = K->variants[vi];
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  auto it = K->mods.find(dev);
-  if (it != K->mods.end()) {
+  auto it = V.mods.find(dev);
+  if (it != V.mods.end()) {
     *out = &it->second;
     return 0;
   }
@@ -511,11 +529,11 @@ int get_mod(lope_kernel* K, DevMod** out) {
   if (!d.ok) return fail(-3, "CUDA driver API unavailable: %s", d.why.c_str());
   CUDA_TRY(cudaFree(nullptr));   // make the primary context current on this thread
   DevMod m;
-  CUresult r = d.moduleLoadData(&m.mod, K->cubin.data());
+  CUresult r = d.moduleLoadData(&m.mod, V.cubin.data());
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleLoadData");
   r = d.moduleGetFunction(&m.generic, m.mod, "lope_generic");
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_generic)");
-  if (K->tiled_ok) {
+  if (V.tiled_ok) {
     r = d.moduleGetFunction(&m.tiled, m.mod, "lope_tiled");
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_tiled)");
     CUdeviceptr gp;
@@ -536,8 +554,27 @@ int get_mod(lope_kernel* K, DevMod** out) {
     if (nb < 1) return fail(-4, "tiled kernel cannot be resident (smem %d B)", m.tiled_smem);
     m.tiled_blocks = nb;
   }
-  K->mods[dev] = m;
-  *out = &K->mods[dev];
+  V.mods[dev] = m;
+  *out = &V.mods[dev];
+  return 0;
+}
+
+// Compile (or fetch from the cubin cache) one specialisation; returns its index in *vi.
+int add_variant(lope_kernel* K, const TileCfg& cfg, int* vi = nullptr) {
+  for (size_t i = 0; i < K->variants.size(); ++i) {
+    const TileCfg& c = K->variants[i].tile;
+    if (c.bxw == cfg.bxw && c.wy == cfg.wy && c.ry == cfg.ry && c.ns == cfg.ns && c.mb == cfg.mb && c.pw == cfg.pw) {
+      if (vi) *vi = (int)i;
+      return 0;
+    }
+  }
+  LopeVariant V;
+  V.tile = cfg;
+  V.tiled_ok = K->ir.rank >= 2 && K->ir.arrays.size() == 1 && tiled_smem_bytes(K->ir, K->dtype, cfg) <= 225 * 1024;
+  V.source = build_source(K, V);
+  if (int e = nvrtc_compile(V.source, "lope_" + K->ir.name, &V.cubin)) return e;
+  K->variants.push_back(std::move(V));
+  if (vi) *vi = (int)K->variants.size() - 1;
   return 0;
 }
 
@@ -639,12 +676,33 @@ int zchunk_default(const lope::Kir& k) {
 }
 
 // Launch the body kernel over `ranges` (0-based start r0, extents ext) of array set.
+std::string plan_key(const lope_layout* L, int wrap) {
+  char b[256];
+  std::snprintf(b, sizeof b, "%d:%lld,%lld,%lld:%d,%d,%d:%d,%d,%d:%d", L->rank, (long long)L->interior[0],
+                (long long)L->interior[1], (long long)L->interior[2], L->lo[0], L->lo[1], L->lo[2], L->hi[0],
+                L->hi[1], L->hi[2], wrap);
+  return b;
+}
+
+// vi / zc: the variant and z-chunk to use; vi < 0 picks the tuned plan for this
+// geometry, or the defaults when it was never tuned.
 template <class T>
 int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const int ext[3],
              const void* const* in, void* const* out, const double* rs, const int64_t* is, int wrap,
-             cudaStream_t st) {
+             cudaStream_t st, int vi = -1, int zc = 0) {
+  if (vi < 0) {
+    vi = 0;
+    if (!K->plans.empty()) {
+      auto it = K->plans.find(plan_key(&layouts[0], wrap));
+      if (it != K->plans.end()) {
+        vi = it->second.variant;
+        zc = it->second.zchunk;
+      }
+    }
+  }
+  const LopeVariant& V = K->variants[vi];
   DevMod* m = nullptr;
-  if (int e = get_mod(K, &m)) return e;
+  if (int e = get_mod(K, vi, &m)) return e;
   const lope::Kir& k = K->ir;
   HScal<T> sc = make_scal<T>(k, rs, is);
   HGeom g;
@@ -657,7 +715,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     g.hi[d] = layouts[0].hi[d];
   }
   g.wrap = wrap;
-  g.zchunk = zchunk_default(k);
+  g.zchunk = zc > 0 ? zc : zchunk_default(k);
   const int vx = 16 / (int)sizeof(T);
   {
     const int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
@@ -677,7 +735,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     for (int d = 1; d < 3; ++d)
       if ((wrap >> d) & 1) geom_ok = geom_ok && L0.interior[d] >= L0.lo[d] + L0.hi[d];
   }
-  const bool use_tiled = K->tiled_ok && k.arrays.size() == 1 && geom_ok &&
+  const bool use_tiled = V.tiled_ok && k.arrays.size() == 1 && geom_ok &&
                          !std::getenv("LOPE_FORCE_GENERIC");
   if (use_tiled) {
     const lope_layout* L = &layouts[0];
@@ -690,7 +748,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     a.s2 = L->stride[2];
     a.org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
             (long long)(L->lo[2] + r0[2]) * L->stride[2];
-    const TileCfg& c = K->tile;
+    const TileCfg& c = V.tile;
     long long ntx = (ext[0] + 32 * vx * c.bxw - 1) / (32 * vx * c.bxw);
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
@@ -869,13 +927,8 @@ int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kerne
   std::string err = lope::parse_kir(text, &K->ir);
   if (!err.empty()) return fail(104, "kernel IR rejected: %s", err.c_str());
   K->dtype = dtype;
-  K->tile = pick_tile(K->ir, dtype);
-  K->tiled_ok = K->ir.rank >= 2 && K->ir.arrays.size() == 1 &&
-                tiled_smem_bytes(K->ir, dtype, K->tile) <= 225 * 1024;
-  K->source = build_source(K.get());
-  std::string nm = "lope_" + K->ir.name;
-  if (int e = nvrtc_compile(K->source, nm, &K->cubin)) return e;
-  K->describe_path = K->tiled_ok ? "tiled_tma" : "generic";
+  if (int e = add_variant(K.get(), pick_tile(K->ir, dtype))) return e;
+  K->describe_path = K->tiled_ok() ? "tiled_tma" : "generic";
   *out = K.release();
   return 0;
 }
@@ -883,8 +936,9 @@ int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kerne
 int lope_kernel_destroy(lope_kernel* k) {
   if (!k) return 0;
   Drv& d = drv();
-  for (auto& kv : k->mods)
-    if (kv.second.mod && d.ok) d.moduleUnload(kv.second.mod);
+  for (auto& v : k->variants)
+    for (auto& kv : v.mods)
+      if (kv.second.mod && d.ok) d.moduleUnload(kv.second.mod);
   delete k;
   return 0;
 }
@@ -907,9 +961,19 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
     for (int d = 0; d < ir.rank; ++d) o << (d ? "," : "") << "[" << ir.fn[a][d] << "," << ir.fp[a][d] << "]";
     o << "]";
   }
-  o << "],\"path\":\"" << k->describe_path << "\",\"tile\":[" << k->tile.bxw << "," << k->tile.wy << ","
-    << k->tile.ry << "," << k->tile.ns << "],\"ctas_per_sm\":" << k->tile.mb << ",\"producer_warp\":"
-    << k->tile.pw << ",\"reads\":" << ir.nreads << "}";
+  const TileCfg& t = k->tile();
+  o << "],\"path\":\"" << k->describe_path << "\",\"tile\":[" << t.bxw << "," << t.wy << "," << t.ry << ","
+    << t.ns << "],\"ctas_per_sm\":" << t.mb << ",\"producer_warp\":" << t.pw << ",\"reads\":" << ir.nreads
+    << ",\"plans\":{";
+  bool first = true;
+  for (const auto& kv : k->plans) {
+    const TileCfg& c = k->variants[kv.second.variant].tile;
+    o << (first ? "" : ",") << "\"" << kv.first << "\":{\"tile\":[" << c.bxw << "," << c.wy << "," << c.ry << ","
+      << c.ns << "],\"producer_warp\":" << c.pw << ",\"zchunk\":" << kv.second.zchunk << ",\"ms\":" << kv.second.ms
+      << "}";
+    first = false;
+  }
+  o << "}}";
   std::string s = o.str();
   if (s.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", s.size() + 1);
   std::memcpy(buf, s.c_str(), s.size() + 1);
@@ -918,8 +982,9 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
 
 int lope_kernel_source(const lope_kernel* k, char* buf, size_t n) {
   if (!k || !buf) return fail(108, "null argument");
-  if (k->source.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", k->source.size() + 1);
-  std::memcpy(buf, k->source.c_str(), k->source.size() + 1);
+  const std::string& src = k->variants[0].source;
+  if (src.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", src.size() + 1);
+  std::memcpy(buf, src.c_str(), src.size() + 1);
   return 0;
 }
 
@@ -1021,6 +1086,83 @@ int lope_step_planes(const lope_kernel* kc, const lope_layout* layout, const voi
   cudaStream_t st = (cudaStream_t)stream;
   return k->dtype == LOPE_F32 ? run_body<float>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st)
                               : run_body<double>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Candidate (variant, z-chunk) plans (lope_plan_candidates).  3-D: the default in-band-producer
+// variant with long z-chunks (past planes live in registers for many planes), and
+// dedicated-producer variants with short z-chunks (neighbouring units overlap in L2,
+// the 2-D regime) at several ring depths.  The best one depends on the geometry and
+// is not monotone in any single parameter (B200, lap3d7 1024^3: 1.40 .. 1.96 ms).
+std::vector<std::pair<TileCfg, int>> tune_candidates(const lope_kernel* K) {
+  std::vector<std::pair<TileCfg, int>> c;
+  const TileCfg base = K->variants[0].tile;
+  if (K->ir.rank == 3) {
+    for (int zc : {16, 32, 64}) c.push_back({base, zc});
+    for (int ns : {8, 10, 12}) {
+      TileCfg t = base;
+      t.pw = 1;
+      t.ns = ns;
+      for (int zc : {3, 4, 6, 8}) c.push_back({t, zc});
+    }
+  } else {
+    c.push_back({base, 1});
+    for (int ns : {8, 12}) {
+      TileCfg t = base;
+      t.ns = ns;
+      t.pw = 1 - base.pw;
+      c.push_back({t, 1});
+    }
+  }
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lope_kernel_prepare(lope_kernel* k) {
+  if (!k) return fail(108, "null argument");
+  if (!k->tiled_ok()) return 0;
+  for (const auto& cand : tune_candidates(k))
+    if (int e = add_variant(k, cand.first)) return e;
+  return 0;
+}
+
+int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, int32_t cap, int32_t* n) {
+  if (!k || !n) return fail(108, "null argument");
+  *n = 0;
+  if (!k->tiled_ok()) return 0;
+  for (const auto& cand : tune_candidates(k)) {
+    int vi = 0;
+    if (int e = add_variant(k, cand.first, &vi)) return e;
+    if (!k->variants[vi].tiled_ok) continue;
+    if (*n < cap && variants && zchunks) {
+      variants[*n] = vi;
+      zchunks[*n] = cand.second;
+    }
+    ++*n;
+  }
+  return 0;
+}
+
+int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk) {
+  if (!k || !layout) return fail(108, "null argument");
+  if (int e = check_layout(layout)) return e;
+  const std::string key = plan_key(layout, wrap_mask & ((1 << k->ir.rank) - 1));
+  if (variant < 0) {
+    k->plans.erase(key);
+    return 0;
+  }
+  if (variant >= (int32_t)k->variants.size()) return fail(108, "no plan variant %d", variant);
+  LopePlan p;
+  p.variant = variant;
+  p.zchunk = zchunk;
+  k->plans[key] = p;
+  return 0;
 }
 
 int lope_halo_fill(const lope_layout* layout, void* buf, int32_t dims_mask, void* stream) {

@@ -216,6 +216,16 @@ class SlabStepper:
     def step(self) -> None:
         import torch
         blk = self.arr.block
+        tuner = self.kernel.tuner(blk, self.arr.local_mask)
+        if tuner is not None:
+            tuner.before()
+        self._step()
+        if tuner is not None:
+            tuner.after()
+
+    def _step(self) -> None:
+        import torch
+        blk = self.arr.block
         src, dst = blk.data, blk.spare()
         cs = torch.cuda.current_stream()
         if self.arr.size == 1:
@@ -240,6 +250,14 @@ class SlabStepper:
             self.arr.exchanger.exchange(dst, blk.layout, cs)
             self._planes(src, dst, b_lo_end, b_hi_beg, cs)
         blk.swap()
+
+    def tune(self) -> int:
+        """Run real steps until the plan for this slab is chosen; returns the count."""
+        n = 0
+        while self.kernel.tuner(self.arr.block, self.arr.local_mask) is not None:
+            self.step()
+            n += 1
+        return n
 
     def iterate(self, steps: int) -> None:
         """``do it = 1, steps; HALO_TRANSFER; launch`` with exact reference end state."""

@@ -26,6 +26,7 @@ copies only); every computation is a liblope_b200.so kernel.
 from __future__ import annotations
 
 import ctypes
+import json
 from typing import Dict, Iterable, Optional, Sequence
 
 import numpy as np
@@ -171,6 +172,94 @@ class HaloArray:
         return int(np.prod(self.interior)) * int(self.layout.elem_bytes)
 
 
+_AUTOTUNE_MIN_CELLS = 1 << 25      # ~128 MB fp32: below this the defaults are within noise
+
+
+def _autotune_enabled() -> bool:
+    import os
+    return os.environ.get("LOPE_AUTOTUNE", "1") not in ("0", "")
+
+
+def _tune_key(arr, mask):
+    L = arr.layout
+    return (tuple(L.interior[:3]), tuple(L.lo[:3]), tuple(L.hi[:3]), int(mask))
+
+
+class PlanTuner:
+    """Online choice of the tiled kernel's execution plan for one geometry.
+
+    The candidates (compiled tile variants x z-chunks, ``lope_plan_candidates``)
+    compute identical bits, so real steps double as measurements: each candidate
+    runs ``STEPS`` consecutive steps (both ping-pong directions, as in steady
+    state), timed with CUDA events on the launching stream, in ``PASSES``
+    round-robin passes; the fastest pass wins and becomes the plan
+    (``lope_plan_set``).  Timing a candidate on repeated launches in one direction
+    ranks the plans differently (measured on B200), hence real alternating steps.
+    """
+
+    STEPS = 2
+    PASSES = 2
+
+    def __init__(self, kernel: "CompiledKernel", layout, wrap_mask: int):
+        self.kernel = kernel
+        self.layout = layout
+        self.mask = int(wrap_mask)
+        cap = 64
+        v, z, n = (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)(), ctypes.c_int32()
+        _lib.check(_lib.lib().lope_plan_candidates(kernel.handle, v, z, cap, ctypes.byref(n)),
+                   "lope_plan_candidates")
+        self.cands = [(int(v[i]), int(z[i])) for i in range(min(n.value, cap))]
+        self.trials = [c for _ in range(self.PASSES) for c in range(len(self.cands))]
+        self.pos = 0
+        self.sub = 0
+        self.timed = []              # (candidate index, start event, end event)
+        self._start = None
+        self.report = {"candidates": [], "best": None}
+        self.done = len(self.cands) <= 1
+
+    @property
+    def steps_needed(self) -> int:
+        return len(self.trials) * self.STEPS
+
+    def _set(self, variant: int, zchunk: int) -> None:
+        _lib.check(_lib.lib().lope_plan_set(self.kernel.handle, ctypes.byref(self.layout), self.mask,
+                                            variant, zchunk), "lope_plan_set")
+
+    def before(self, stream=None) -> None:
+        if self.sub == 0:
+            self._set(*self.cands[self.trials[self.pos]])
+            self._start = _torch().cuda.Event(enable_timing=True)
+            self._start.record(stream)
+
+    def after(self, stream=None) -> None:
+        self.sub += 1
+        if self.sub < self.STEPS:
+            return
+        end = _torch().cuda.Event(enable_timing=True)
+        end.record(stream)
+        self.timed.append((self.trials[self.pos], self._start, end))
+        self.sub = 0
+        self.pos += 1
+        if self.pos == len(self.trials):
+            self._finish()
+
+    def _finish(self) -> None:
+        self.timed[-1][2].synchronize()
+        best = {}
+        for c, a, b in self.timed:
+            ms = a.elapsed_time(b) / self.STEPS
+            best[c] = min(best.get(c, ms), ms)
+        ci = min(best, key=best.get)
+        self._set(*self.cands[ci])
+        desc = json.loads(self.kernel.describe())
+        self.report = {"candidates": [[self.cands[c][0], self.cands[c][1], round(best[c], 5)] for c in sorted(best)],
+                       "best": {"variant": self.cands[ci][0], "zchunk": self.cands[ci][1],
+                                "ms_per_step": round(best[ci], 5)},
+                       "plans": desc.get("plans")}
+        self.timed = []
+        self.done = True
+
+
 class CompiledKernel:
     """A locally-oriented kernel compiled for sm_100a (``lope_kernel_compile``)."""
 
@@ -188,6 +277,7 @@ class CompiledKernel:
         self.text = text
         self.dtype_code = _lib.dtype_code(dtype)
         self.handle = _lib.compile_kernel(text, self.dtype_code)
+        self._tuners = {}
 
     def __del__(self):
         try:
@@ -200,6 +290,33 @@ class CompiledKernel:
 
     def source(self) -> str:
         return _lib.source(self.handle)
+
+    def tuner(self, arr: "HaloArray", wrap_mask: int) -> Optional["PlanTuner"]:
+        """The online plan tuner for ``arr``'s geometry while it is still measuring
+        (None once a plan is chosen, for small blocks, with ``LOPE_AUTOTUNE=0`` and
+        during CUDA-graph capture)."""
+        key = _tune_key(arr, wrap_mask)
+        t = self._tuners.get(key)
+        if t is None:
+            if not _autotune_enabled() or arr.layout.count < _AUTOTUNE_MIN_CELLS:
+                return None
+            t = self._tuners[key] = PlanTuner(self, arr.layout, wrap_mask)
+        if t.done or _torch().cuda.is_current_stream_capturing():
+            return None
+        return t
+
+    def tune(self, arr: "HaloArray", scalars=None, wrap_mask: Optional[int] = None, stream=None) -> dict:
+        """Choose the plan for ``arr``'s geometry now by running real fused steps under
+        each candidate (this advances the field by ``PlanTuner.steps_needed`` steps --
+        the bits are the same whichever plan runs them).  Returns the tuning report."""
+        mask = (1 << arr.rank) - 1 if wrap_mask is None else wrap_mask
+        key = _tune_key(arr, mask)
+        t = self._tuners.get(key)
+        if t is None:
+            t = self._tuners[key] = PlanTuner(self, arr.layout, mask)
+        while not t.done:
+            step(self, arr, scalars, mask, stream)
+        return t.report
 
     def scalar_args(self, scalars: Optional[Dict[str, float]]):
         scalars = scalars or {}
@@ -262,12 +379,17 @@ def step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Option
          stream=None) -> None:
     """Fused launch (full interior) + the following HALO_TRANSFER's local fill."""
     mask = (1 << arr.rank) - 1 if wrap_mask is None else wrap_mask
+    tuner = kernel.tuner(arr, mask)
+    if tuner is not None:
+        tuner.before(stream)
     rs, is_ = kernel.scalar_args(scalars)
     _lib.check(_lib.lib().lope_step(kernel.handle, ctypes.byref(arr.layout),
                                     ctypes.c_void_p(arr.data.data_ptr()),
                                     ctypes.c_void_p(arr.spare().data_ptr()), rs, is_, mask,
                                     ctypes.c_void_p(_stream_handle(stream))), "lope_step")
     arr.swap()
+    if tuner is not None:
+        tuner.after(stream)
 
 
 def iterate(kernel: CompiledKernel, arr: HaloArray, steps: int, scalars=None, stream=None) -> None:

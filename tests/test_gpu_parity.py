@@ -263,3 +263,30 @@ def test_full_size_multi_step_tiled_equals_generic(monkeypatch):
                        b.padded_view().contiguous().view(torch.int32))
     del a, b
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name,shape,dt", [("lap3d7", (256, 96, 64), "float32"),
+                                           ("ninept2d", (512, 256), "float32"),
+                                           ("box5x5", (256, 128), "float64")])
+def test_plan_tuning_is_bitwise_transparent(name, shape, dt):
+    """The online tuner runs real steps under every candidate plan and keeps one;
+    the field after tuning plus further steps equals the plain run of as many steps."""
+    import json
+    kir = stencils.by_name(name)
+    npdt = np.float32 if dt == "float32" else np.float64
+    field = O.hash_field(shape, 23, npdt)
+    k = R.CompiledKernel(kir, dt)
+    l_, h_ = halos_of(kir)
+    arr = R.HaloArray(shape, l_, h_, dt)
+    arr.set_interior(field)
+    R.halo_transfer(arr)
+    rep = k.tune(arr)
+    t = k._tuners[next(iter(k._tuners))]
+    n_tune = t.steps_needed if len(t.cands) > 1 else 0
+    assert rep["best"] is not None or len(t.cands) <= 1
+    if len(t.cands) > 1:
+        assert len(json.loads(k.describe())["plans"]) == 1
+    R.step(k, arr)
+    R.launch(k, [arr])
+    plain = gpu_iterate(kir, field, n_tune + 2, {}, dt).get_interior()
+    assert O.equal_bits(arr.get_interior(), plain)

@@ -1,6 +1,8 @@
 """Debug: time lope_step on the c3 workload under different tile/zchunk/grid settings."""
 import os, sys, pathlib, subprocess, json
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+if os.environ.get("TUNE") != "1":
+    os.environ["LOPE_AUTOTUNE"] = "0"      # env overrides below are the experiment
 import torch
 from paper_1502_03504_b200 import runtime as R, stencils
 shape = tuple(int(x) for x in os.environ.get("SHAPE", "1024,1024,1024").split(","))
@@ -40,6 +42,9 @@ R.halo_transfer(a)
 for _ in range(3):
     R.step(k, a)
 torch.cuda.synchronize()
+import numpy as np
+if os.environ.get("TUNE") == "1":
+    print("tune", json.dumps(k.tune(a)), file=sys.stderr)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n = int(os.environ.get("N", "10"))
 e0.record()
@@ -54,6 +59,13 @@ for _ in range(n):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / n
+if os.environ.get("ALT") == "1":
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
+        ev[i][0].record(); R.step(k, a); ev[i][1].record()
+    torch.cuda.synchronize()
+    t = [x.elapsed_time(y) for x, y in ev]
+    print("alt even/odd ms", round(float(np.median(t[0::2])), 4), round(float(np.median(t[1::2])), 4), file=sys.stderr)
 import numpy as np
 pts = np.prod(shape)
 esz = 4 if dt == "float32" else 8
