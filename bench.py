@@ -105,6 +105,8 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples = []
+        self.power = []
+        self.mem_mhz = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -125,6 +127,8 @@ class ClockSampler:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
+                self.mem_mhz.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_MEM))
             except Exception:
                 pass
             time.sleep(0.002)
@@ -147,7 +151,11 @@ class ClockSampler:
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
         reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s)}
+        p = sorted(self.power)
+        mm = sorted(self.mem_mhz)
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s),
+                "power_w_median": round(p[len(p) // 2], 1) if p else None,
+                "mem_mhz_median": mm[len(mm) // 2] if mm else None}
 
 
 # ---------------------------------------------------------------------------

@@ -134,15 +134,17 @@ int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const i
  * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
  * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */
 /* Execution plans (which compiled tile variant, which z-chunk) for the tiled kernel.
- * lope_plan_candidates compiles the candidate variants and lists (variant, z-chunk)
- * pairs (n = how many exist; at most `cap` are written).  lope_plan_set makes one of
+ * lope_plan_candidates compiles the candidate variants and lists (variant, z-chunk,
+ * y-band of the unit walk) triples (n = how many exist; at most `cap` are written).  lope_plan_set makes one of
  * them the plan for every later launch whose first layout has this interior, halos
  * and wrap mask (variant -1 clears it).  Every plan computes the same bits; the host
  * runtime times real steps under each candidate and keeps the fastest. */
 /* Compile every plan variant (NVRTC, cached; no GPU needed). */
 int lope_kernel_prepare(lope_kernel* k);
-int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, int32_t cap, int32_t* n);
-int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk);
+int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, int32_t* ybands, int32_t cap,
+                         int32_t* n);
+int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk,
+                  int32_t yband);
 
 /* Box <-> contiguous device buffer (column-major within the box, dim 1 fastest):
  * `extent` cells at padded coordinates `lo`.  Faces of a decomposed dimension other

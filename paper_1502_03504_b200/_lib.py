@@ -71,8 +71,8 @@ def lib():
     L.lope_unpack_padded.argtypes = [P(Layout), VP, VP, VP]
     L.lope_copy_box.argtypes = [P(Layout), VP, VP, P(I64), P(I64), P(I64), VP]
     L.lope_kernel_prepare.argtypes = [VP]
-    L.lope_plan_candidates.argtypes = [VP, P(I32), P(I32), I32, P(I32)]
-    L.lope_plan_set.argtypes = [VP, P(Layout), I32, I32, I32]
+    L.lope_plan_candidates.argtypes = [VP, P(I32), P(I32), P(I32), I32, P(I32)]
+    L.lope_plan_set.argtypes = [VP, P(Layout), I32, I32, I32, I32]
     L.lope_box_pack.argtypes = [P(Layout), VP, P(I64), P(I64), VP, VP]
     L.lope_box_unpack.argtypes = [P(Layout), VP, P(I64), P(I64), VP, VP]
     L.lope_fill_hash.argtypes = [P(Layout), VP, ctypes.c_uint64, P(I64), P(I64), VP]

@@ -304,7 +304,7 @@ template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
 template <class T> struct HScal { T v[LOPE_HOST_MAX_SCAL]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
-  int wrap, zchunk, xshift, box0, p1;
+  int wrap, zchunk, xshift, box0, p1, yband;
 };
 
 }  // namespace
@@ -322,6 +322,7 @@ struct LopeVariant {
 struct LopePlan {
   int variant = 0;
   int zchunk = 0;
+  int yband = 0;
   double ms = 0.0;
 };
 
@@ -689,7 +690,7 @@ std::string plan_key(const lope_layout* L, int wrap) {
 template <class T>
 int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const int ext[3],
              const void* const* in, void* const* out, const double* rs, const int64_t* is, int wrap,
-             cudaStream_t st, int vi = -1, int zc = 0) {
+             cudaStream_t st, int vi = -1, int zc = 0, int yband = 0) {
   if (vi < 0) {
     vi = 0;
     if (!K->plans.empty()) {
@@ -697,6 +698,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
       if (it != K->plans.end()) {
         vi = it->second.variant;
         zc = it->second.zchunk;
+        yband = it->second.yband;
       }
     }
   }
@@ -716,6 +718,8 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   }
   g.wrap = wrap;
   g.zchunk = zc > 0 ? zc : zchunk_default(k);
+  g.yband = yband;
+  if (const char* e = std::getenv("LOPE_YBAND")) g.yband = std::atoi(e);
   const int vx = 16 / (int)sizeof(T);
   {
     const int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
@@ -969,7 +973,7 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
   for (const auto& kv : k->plans) {
     const TileCfg& c = k->variants[kv.second.variant].tile;
     o << (first ? "" : ",") << "\"" << kv.first << "\":{\"tile\":[" << c.bxw << "," << c.wy << "," << c.ry << ","
-      << c.ns << "],\"producer_warp\":" << c.pw << ",\"zchunk\":" << kv.second.zchunk << ",\"ms\":" << kv.second.ms
+      << c.ns << "],\"producer_warp\":" << c.pw << ",\"zchunk\":" << kv.second.zchunk << ",\"yband\":" << kv.second.yband
       << "}";
     first = false;
   }
@@ -1097,24 +1101,30 @@ namespace {
 // dedicated-producer variants with short z-chunks (neighbouring units overlap in L2,
 // the 2-D regime) at several ring depths.  The best one depends on the geometry and
 // is not monotone in any single parameter (B200, lap3d7 1024^3: 1.40 .. 1.96 ms).
-std::vector<std::pair<TileCfg, int>> tune_candidates(const lope_kernel* K) {
-  std::vector<std::pair<TileCfg, int>> c;
+struct PlanCand {
+  TileCfg tile;
+  int zchunk, yband;
+};
+
+std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
+  std::vector<PlanCand> c;
   const TileCfg base = K->variants[0].tile;
   if (K->ir.rank == 3) {
-    for (int zc : {16, 32, 64}) c.push_back({base, zc});
+    for (int zc : {16, 32, 64}) c.push_back({base, zc, 0});
     for (int ns : {8, 10, 12}) {
       TileCfg t = base;
       t.pw = 1;
       t.ns = ns;
-      for (int zc : {3, 4, 6, 8}) c.push_back({t, zc});
+      // (y-banded walks, yband 4-16, measured no better on 1024^3 / 2048^3)
+      for (int zc : {3, 4, 6, 8}) c.push_back({t, zc, 0});
     }
   } else {
-    c.push_back({base, 1});
+    c.push_back({base, 1, 0});
     for (int ns : {8, 12}) {
       TileCfg t = base;
       t.ns = ns;
       t.pw = 1 - base.pw;
-      c.push_back({t, 1});
+      c.push_back({t, 1, 0});
     }
   }
   return c;
@@ -1128,28 +1138,31 @@ int lope_kernel_prepare(lope_kernel* k) {
   if (!k) return fail(108, "null argument");
   if (!k->tiled_ok()) return 0;
   for (const auto& cand : tune_candidates(k))
-    if (int e = add_variant(k, cand.first)) return e;
+    if (int e = add_variant(k, cand.tile)) return e;
   return 0;
 }
 
-int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, int32_t cap, int32_t* n) {
+int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, int32_t* ybands, int32_t cap,
+                         int32_t* n) {
   if (!k || !n) return fail(108, "null argument");
   *n = 0;
   if (!k->tiled_ok()) return 0;
   for (const auto& cand : tune_candidates(k)) {
     int vi = 0;
-    if (int e = add_variant(k, cand.first, &vi)) return e;
+    if (int e = add_variant(k, cand.tile, &vi)) return e;
     if (!k->variants[vi].tiled_ok) continue;
-    if (*n < cap && variants && zchunks) {
+    if (*n < cap && variants && zchunks && ybands) {
       variants[*n] = vi;
-      zchunks[*n] = cand.second;
+      zchunks[*n] = cand.zchunk;
+      ybands[*n] = cand.yband;
     }
     ++*n;
   }
   return 0;
 }
 
-int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk) {
+int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk,
+                  int32_t yband) {
   if (!k || !layout) return fail(108, "null argument");
   if (int e = check_layout(layout)) return e;
   const std::string key = plan_key(layout, wrap_mask & ((1 << k->ir.rank) - 1));
@@ -1161,6 +1174,7 @@ int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, 
   LopePlan p;
   p.variant = variant;
   p.zchunk = zchunk;
+  p.yband = yband;
   k->plans[key] = p;
   return 0;
 }

@@ -166,6 +166,7 @@ struct LopeGeom {
   int xshift;     // tiled: elements the TMA box starts early so its start is 16-byte aligned
   int box0;       // tiled: TMA x coordinate of tile 0's box (row-relative, already shifted)
   int p1;         // tiled: padded rows per plane; > 0 selects the flattened 2-D tensor map
+  int yband;      // tiled: tile rows per band of the unit walk (0: whole plane)
 };
 
 // --------------------------------------------------------------------------
@@ -417,20 +418,29 @@ __device__ __forceinline__ void lope_mbar_arrive(lope_u64* bar) {
 // their edges (and the halo rows) are fetched from HBM once and hit in L2 for the
 // neighbour.  The host picks G with G % ntx != 0 so x-edge tiles rotate over CTAs.
 struct LopeUnitWalk {
-  int tx, ty, zi, gtx, gty, gzi, ntx, nty;
-  __device__ __forceinline__ void init(int b, int G, int nty_, int ntx_) {
-    nty = nty_; ntx = ntx_;
-    tx = b % ntx; int r = b / ntx; ty = r % nty; zi = r / nty;
-    gtx = G % ntx; r = G / ntx; gty = r % nty; gzi = r / nty;
+  // Unit index -> (tx, ty, zi) in the mixed radix (tx: ntx, ty_lo: yb, zi: nzc,
+  // ty_hi: nty/yb), x fastest.  yb = nty is the plain x-y-z order; a smaller band
+  // puts the next z-chunk of a tile only ntx*yb units later (its halo planes are
+  // still in L2) at the cost of y-halo reuse across band edges.  Advanced by the
+  // grid stride with carries (no division per unit).
+  int tx, tyl, zi, tyh, gtx, gtyl, gzi, gtyh, ntx, yb, nzc;
+  __device__ __forceinline__ void init(int b, int G, int ntx_, int yb_, int nzc_) {
+    ntx = ntx_; yb = yb_; nzc = nzc_;
+    tx = b % ntx; int r = b / ntx; tyl = r % yb; r /= yb; zi = r % nzc; tyh = r / nzc;
+    gtx = G % ntx; r = G / ntx; gtyl = r % yb; r /= yb; gzi = r % nzc; gtyh = r / nzc;
   }
+  __device__ __forceinline__ int ty() const { return tyh * yb + tyl; }
   __device__ __forceinline__ void next() {
     tx += gtx;
     int c = 0;
     if (tx >= ntx) { tx -= ntx; c = 1; }
-    ty += gty + c;
+    tyl += gtyl + c;
     c = 0;
-    if (ty >= nty) { ty -= nty; c = 1; }
+    if (tyl >= yb) { tyl -= yb; c = 1; }
     zi += gzi + c;
+    c = 0;
+    if (zi >= nzc) { zi -= nzc; c = 1; }
+    tyh += gtyh + c;
   }
 };
 
@@ -454,13 +464,7 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int zc = g.zchunk;
   const int nzc = (g.ext[2] + zc - 1) / zc;
   const int nunits = ntx * nty * nzc;     // < 2^31 (host checks)
-#ifdef LOPE_WALK_ZY
-  // experiment: walk x, then z-chunk, then y (y neighbours a whole x-z sweep apart)
-  constexpr bool ZY = true;
-#else
-  constexpr bool ZY = false;
-#endif
-  const int nmid = ZY ? nzc : nty;
+const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -493,12 +497,12 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int oz = g.lo[2] + g.r0[2] - FZN;
   const int pwarp = PW ? C::NCW : 0;     // the warp that issues TMA
   if (warp == pwarp && lane == 0) {
-    pw.init(blockIdx.x, gridDim.x, nmid, ntx);
+    pw.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
     if (p_u < nunits) {
-      const int z0 = (ZY ? pw.ty : pw.zi) * zc;
+      const int z0 = pw.zi * zc;
       p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
       p_bx = g.box0 + pw.tx * C::BX;
-      p_by = oy + (ZY ? pw.zi : pw.ty) * C::BY;
+      p_by = oy + pw.ty() * C::BY;
       p_z = oz + z0;
     }
   }
@@ -506,7 +510,7 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
     while (p_L < limit && p_u < nunits) {
 #ifdef LOPE_STAGGER2
       // experiment: delay the first load of odd-parity tiles' units
-      if (p_pl == 0 && ((pw.tx + pw.ty) & 1)) {
+      if (p_pl == 0 && ((pw.tx + pw.ty()) & 1)) {
         lope_u64 t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < (lope_u64)(LOPE_STAGGER2));
@@ -525,10 +529,10 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
         p_u += gridDim.x;
         pw.next();
         if (p_u < nunits) {
-          const int z0 = (ZY ? pw.ty : pw.zi) * zc;
+          const int z0 = pw.zi * zc;
           p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
           p_bx = g.box0 + pw.tx * C::BX;
-          p_by = oy + (ZY ? pw.zi : pw.ty) * C::BY;
+          p_by = oy + pw.ty() * C::BY;
           p_z = oz + z0;
         }
       }
@@ -554,14 +558,14 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
 
   LopeUnitWalk w;
-  w.init(blockIdx.x, gridDim.x, nmid, ntx);
+  w.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
   lope_u32 lbase = 0;
   T hist[FZN > 0 ? FZN : 1][RY][VX];
   for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
-    const int z0 = (ZY ? w.ty : w.zi) * zc;
+    const int z0 = w.zi * zc;
     const int nz = min(zc, g.ext[2] - z0);
     const int x = w.tx * C::BX + cx;
-    const int ybase = (ZY ? w.zi : w.ty) * C::BY + row0;
+    const int ybase = w.ty() * C::BY + row0;
     const bool xok = x < g.ext[0];
     const int nrow = min(RY, g.ext[1] - ybase);
     // Periodic images (lope_step): x images are whole 64-byte atoms written by the

@@ -205,10 +205,10 @@ class PlanTuner:
         self.layout = layout
         self.mask = int(wrap_mask)
         cap = 64
-        v, z, n = (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)(), ctypes.c_int32()
-        _lib.check(_lib.lib().lope_plan_candidates(kernel.handle, v, z, cap, ctypes.byref(n)),
+        v, z, y, n = (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)(), ctypes.c_int32()
+        _lib.check(_lib.lib().lope_plan_candidates(kernel.handle, v, z, y, cap, ctypes.byref(n)),
                    "lope_plan_candidates")
-        self.cands = [(int(v[i]), int(z[i])) for i in range(min(n.value, cap))]
+        self.cands = [(int(v[i]), int(z[i]), int(y[i])) for i in range(min(n.value, cap))]
         self.trials = [c for _ in range(self.PASSES) for c in range(len(self.cands))]
         self.pos = 0
         self.sub = 0
@@ -221,9 +221,9 @@ class PlanTuner:
     def steps_needed(self) -> int:
         return len(self.trials) * self.STEPS
 
-    def _set(self, variant: int, zchunk: int) -> None:
+    def _set(self, variant: int, zchunk: int, yband: int) -> None:
         _lib.check(_lib.lib().lope_plan_set(self.kernel.handle, ctypes.byref(self.layout), self.mask,
-                                            variant, zchunk), "lope_plan_set")
+                                            variant, zchunk, yband), "lope_plan_set")
 
     def before(self, stream=None) -> None:
         if self.sub == 0:
@@ -252,9 +252,9 @@ class PlanTuner:
         ci = min(best, key=best.get)
         self._set(*self.cands[ci])
         desc = json.loads(self.kernel.describe())
-        self.report = {"candidates": [[self.cands[c][0], self.cands[c][1], round(best[c], 5)] for c in sorted(best)],
+        self.report = {"candidates": [list(self.cands[c]) + [round(best[c], 5)] for c in sorted(best)],
                        "best": {"variant": self.cands[ci][0], "zchunk": self.cands[ci][1],
-                                "ms_per_step": round(best[ci], 5)},
+                                "yband": self.cands[ci][2], "ms_per_step": round(best[ci], 5)},
                        "plans": desc.get("plans")}
         self.timed = []
         self.done = True

@@ -126,6 +126,17 @@ def test_tile_schedule_order_invariance(monkeypatch):
         monkeypatch.setenv("LOPE_ZCHUNK", zc)
         got = gpu_iterate(kir, f, 2, {}, "float32").get_interior()
         assert O.equal_bits(got, base), (grid, zc)
+    # banded unit walks (tile rows per band) and producer variants
+    f = O.hash_field((256, 256, 20), 9, np.float32)
+    monkeypatch.delenv("LOPE_GRID")
+    monkeypatch.delenv("LOPE_ZCHUNK")
+    base = gpu_iterate(kir, f, 2, {}, "float32").get_interior()
+    for yb, zc, grid in (("2", "3", "37"), ("4", "1", "147"), ("8", "6", "100"), ("1", "2", "9")):
+        monkeypatch.setenv("LOPE_YBAND", yb)
+        monkeypatch.setenv("LOPE_ZCHUNK", zc)
+        monkeypatch.setenv("LOPE_GRID", grid)
+        got = gpu_iterate(kir, f, 2, {}, "float32").get_interior()
+        assert O.equal_bits(got, base), (yb, zc, grid)
 
 
 def test_halo_transfer_fills_every_padded_cell(golden_exchange):
