@@ -324,7 +324,7 @@ def run_gpu_arm(args, wl):
     launches = _lib.launch_count() - l0
     total_ms = t_all0.elapsed_time(t_all1)
     if graph is not None:
-        launches = steps_done          # one graph replay: the host counter saw the captures
+        launches = graph.launches      # one graph replay: the host counter saw the captures
         per_step = [total_ms / steps_done]
     else:
         per_step = [a.elapsed_time(b) for a, b in ev]

@@ -133,6 +133,13 @@ int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const i
 /* Fill the interior with the synthetic U(-1,1) field: value of global cell
  * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
  * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */
+/* `nsteps` fused steps (lope_step with every dim periodic) alternating between two
+ * buffers, buf0 live first; *live_index = 0 or 1 names the buffer holding the result.
+ * Rank-2 kernels advance 4 steps per launch in shared memory (temporal blocking;
+ * same bits as 4 single steps) when the interior is at least a tile plus 4 halos. */
+int lope_step_multi(const lope_kernel* k, const lope_layout* layout, void* buf0, void* buf1, int64_t nsteps,
+                    const double* rscal, const int64_t* iscal, void* stream, int32_t* live_index);
+
 /* Execution plans (which compiled tile variant, which z-chunk) for the tiled kernel.
  * lope_plan_candidates compiles the candidate variants and lists (variant, z-chunk,
  * y-band of the unit walk) triples (n = how many exist; at most `cap` are written).  lope_plan_set makes one of

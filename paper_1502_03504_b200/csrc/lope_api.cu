@@ -296,6 +296,8 @@ struct DevMod {
   CUfunction generic = nullptr;
   CUfunction tiled = nullptr;
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
+  CUfunction tblock = nullptr;          // temporal blocking (rank 2), variant 0 only
+  int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0;
 };
 
 // host mirrors of the device parameter structs (lope_device.cuh)
@@ -433,7 +435,7 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
   return c;
 }
 
-std::string build_source(const lope_kernel* K, const LopeVariant& V) {
+std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_tblock) {
   const lope::Kir& k = K->ir;
   std::ostringstream s;
   s << kDeviceSrc << "\n";
@@ -455,6 +457,15 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V) {
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
       << ", " << c.pw << ">(&map, a, sc, g);\n}\n";
+  }
+  if (with_tblock && k.rank == 2 && k.arrays.size() == 1) {
+    const int tx = K->dtype == LOPE_F32 ? 128 : 64, ty = 32, tt = 4;
+    s << "typedef LopeTblockCfg<LopeBody, LT, " << tx << ", " << ty << ", " << tt << "> LopeTbCfg;\n";
+    s << "extern \"C\" __constant__ int lope_tblock_info[4] = {LopeTbCfg::SMEM_BYTES, " << tx << ", " << ty << ", "
+      << tt << "};\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(1024) lope_tblock(const LopeArr<LT> a, "
+         "const LopeScal<LT> sc, const LopeGeom g) {\n"
+      << "  lope_tblock_impl<LopeBody, LT, " << tx << ", " << ty << ", " << tt << ">(a, sc, g);\n}\n";
   }
   return s.str();
 }
@@ -555,6 +566,22 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     if (nb < 1) return fail(-4, "tiled kernel cannot be resident (smem %d B)", m.tiled_smem);
     m.tiled_blocks = nb;
   }
+  if (d.moduleGetFunction(&m.tblock, m.mod, "lope_tblock") == CUDA_SUCCESS) {
+    CUdeviceptr gp;
+    size_t gsz;
+    r = d.moduleGetGlobal(&gp, &gsz, m.mod, "lope_tblock_info");
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetGlobal(lope_tblock_info)");
+    int info[4];
+    CUDA_TRY(cudaMemcpy(info, (const void*)gp, sizeof info, cudaMemcpyDeviceToHost));
+    m.tb_smem = info[0];
+    m.tb_tx = info[1];
+    m.tb_ty = info[2];
+    m.tb_tt = info[3];
+    r = d.funcSetAttribute(m.tblock, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tb_smem);
+    if (r != CUDA_SUCCESS) m.tblock = nullptr;
+  } else {
+    m.tblock = nullptr;
+  }
   V.mods[dev] = m;
   *out = &V.mods[dev];
   return 0;
@@ -572,7 +599,7 @@ int add_variant(lope_kernel* K, const TileCfg& cfg, int* vi = nullptr) {
   LopeVariant V;
   V.tile = cfg;
   V.tiled_ok = K->ir.rank >= 2 && K->ir.arrays.size() == 1 && tiled_smem_bytes(K->ir, K->dtype, cfg) <= 225 * 1024;
-  V.source = build_source(K, V);
+  V.source = build_source(K, V, K->variants.empty());
   if (int e = nvrtc_compile(V.source, "lope_" + K->ir.name, &V.cubin)) return e;
   K->variants.push_back(std::move(V));
   if (vi) *vi = (int)K->variants.size() - 1;
@@ -677,6 +704,27 @@ int zchunk_default(const lope::Kir& k) {
 }
 
 // Launch the body kernel over `ranges` (0-based start r0, extents ext) of array set.
+// Launch with programmatic dependent launch when available (see run_body).
+CUresult launch_ex(CUfunction f, unsigned grid, unsigned block, int smem, cudaStream_t st, void** args) {
+  Drv& d = drv();
+  if (d.launchKernelEx && pdl_enabled()) {
+    CUlaunchAttribute at[1];
+    std::memset(at, 0, sizeof at);
+    at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    at[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDimX = grid; cfg.gridDimY = 1; cfg.gridDimZ = 1;
+    cfg.blockDimX = block; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)smem;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return d.launchKernelEx(&cfg, f, args, nullptr);
+  }
+  return d.launchKernel(f, grid, 1, 1, block, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr);
+}
+
 std::string plan_key(const lope_layout* L, int wrap) {
   char b[256];
   std::snprintf(b, sizeof b, "%d:%lld,%lld,%lld:%d,%d,%d:%d,%d,%d:%d", L->rank, (long long)L->interior[0],
@@ -1139,6 +1187,79 @@ int lope_kernel_prepare(lope_kernel* k) {
   if (!k->tiled_ok()) return 0;
   for (const auto& cand : tune_candidates(k))
     if (int e = add_variant(k, cand.tile)) return e;
+  return 0;
+}
+
+int lope_step_multi(const lope_kernel* kc, const lope_layout* layout, void* buf0, void* buf1, int64_t nsteps,
+                    const double* rscal, const int64_t* iscal, void* stream, int32_t* live_index) {
+  lope_kernel* k = const_cast<lope_kernel*>(kc);
+  if (!k || !layout || !live_index) return fail(108, "null argument");
+  if (int e = check_layout(layout)) return e;
+  const lope::Kir& ir = k->ir;
+  if (ir.arrays.size() != 1) return fail(108, "lope_step_multi takes kernels with one array parameter");
+  if (layout->rank != ir.rank || layout->dtype != k->dtype)
+    return fail(108, "layout rank/dtype do not match kernel '%s'", ir.name.c_str());
+  if (!buf0 || !buf1) return fail(202, "buffer not allocated");
+  if (buf0 == buf1) return fail(108, "lope_step_multi needs two distinct buffers");
+  if (nsteps < 0) return fail(108, "negative step count");
+  for (int d = 0; d < 3; ++d)
+    if (ir.fn[0][d] > layout->lo[d] || ir.fp[0][d] > layout->hi[d])
+      return fail(102, "kernel '%s' footprint exceeds the halo in dim %d", ir.name.c_str(), d + 1);
+  if (int e = check_interior_halo(layout)) return e;
+  DevMod* m = nullptr;
+  if (int e = get_mod(k, 0, &m)) return e;
+  const int full = (1 << ir.rank) - 1;
+  const bool tb = m->tblock && ir.rank == 2 && !std::getenv("LOPE_NO_TBLOCK") &&
+                  layout->interior[0] >= m->tb_tx + m->tb_tt * (ir.fn[0][0] + ir.fp[0][0]) &&
+                  layout->interior[1] >= m->tb_ty + m->tb_tt * (ir.fn[0][1] + ir.fp[0][1]);
+  void* bufs[2] = {buf0, buf1};
+  int live = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  Drv& d = drv();
+  // blocks of tb_tt steps plus single steps; the buffer flips once per launch, so
+  // trade one block for tb_tt single steps when that makes the parity match
+  // nsteps -- the result then sits where nsteps single steps would leave it
+  long long nblk = tb ? nsteps / m->tb_tt : 0;
+  if (nblk > 0 && ((nblk + (nsteps - nblk * m->tb_tt)) & 1) != (nsteps & 1)) --nblk;
+  while (nsteps > 0) {
+    if (nblk > 0) {
+      --nblk;
+      const long long ntx = (layout->interior[0] + m->tb_tx - 1) / m->tb_tx;
+      const long long nty = (layout->interior[1] + m->tb_ty - 1) / m->tb_ty;
+      HGeom g;
+      std::memset(&g, 0, sizeof g);
+      for (int dd = 0; dd < 3; ++dd) {
+        g.ext[dd] = (int)layout->interior[dd];
+        g.m[dd] = (int)layout->interior[dd];
+        g.lo[dd] = layout->lo[dd];
+        g.hi[dd] = layout->hi[dd];
+      }
+      g.wrap = full;
+      const long long org = layout->base + layout->lo[0] + (long long)layout->lo[1] * layout->stride[1];
+      CUresult r;
+      if (k->dtype == LOPE_F32) {
+        HArr<float> a{(const float*)bufs[live], (float*)bufs[1 - live], layout->stride[1], layout->stride[2], org};
+        HScal<float> sc = make_scal<float>(ir, rscal, iscal);
+        void* args[] = {&a, &sc, &g};
+        r = launch_ex(m->tblock, (unsigned)(ntx * nty), 1024, m->tb_smem, st, args);
+      } else {
+        HArr<double> a{(const double*)bufs[live], (double*)bufs[1 - live], layout->stride[1], layout->stride[2],
+                       org};
+        HScal<double> sc = make_scal<double>(ir, rscal, iscal);
+        void* args[] = {&a, &sc, &g};
+        r = launch_ex(m->tblock, (unsigned)(ntx * nty), 1024, m->tb_smem, st, args);
+      }
+      if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tblock)");
+      g_launches++;
+      nsteps -= m->tb_tt;
+    } else {
+      if (int e = lope_step(k, layout, bufs[live], bufs[1 - live], rscal, iscal, full, stream)) return e;
+      nsteps -= 1;
+    }
+    live = 1 - live;
+  }
+  (void)d;
+  *live_index = live;
   return 0;
 }
 

@@ -776,3 +776,117 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
     lbase += nz + NZW - 1;
   }
 }
+
+// --------------------------------------------------------------------------
+// Temporal blocking (rank 2, one array, every dim periodic): TT fused steps per
+// launch for fields that live in L2 (config 1), where a launch costs more than its
+// arithmetic.  Each CTA loads its tile plus TT footprints of halo (periodic indices
+// straight from the interior), advances it TT steps in shared memory -- the valid
+// region shrinking by one footprint per step -- and stores the last step's tile and
+// its periodic images.  Every point is evaluated with the same expression on the
+// same operands as the one-step kernel, so the bits are identical.
+
+template <class T, int W>
+struct LopeSmemTile2 {
+  const T* buf;
+  int bx, by;
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ T at() const { return buf[(by + DY) * W + bx + DX]; }
+};
+
+template <class Body, class T, int TX, int TY, int TT>
+struct LopeTblockCfg {
+  static constexpr int WI = TX + TT * (Body::FN0 + Body::FP0);
+  static constexpr int HI = TY + TT * (Body::FN1 + Body::FP1);
+  static constexpr int SMEM_BYTES = 2 * WI * HI * (int)sizeof(T);
+};
+
+template <class Body, class T, int TX, int TY, int TT>
+__device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const LopeScal<T>& sc, const LopeGeom& g) {
+  typedef LopeTblockCfg<Body, T, TX, TY, TT> C;
+  constexpr int FN0 = Body::FN0, FP0 = Body::FP0, FN1 = Body::FN1, FP1 = Body::FP1;
+  constexpr int WI = C::WI, HI = C::HI;
+  constexpr int NTX = TX, NTY = 1024 / TX;         // 1024 threads: a full tile row per row phase
+  extern __shared__ __align__(16) unsigned char lope_smem[];
+  T* b0 = reinterpret_cast<T*>(lope_smem);
+  T* b1 = b0 + WI * HI;
+  const int m0 = g.m[0], m1 = g.m[1];
+  const int ntx = (m0 + TX - 1) / TX;
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const int x0 = tx * TX - TT * FN0, y0 = ty * TY - TT * FN1;   // interior coords of buffer (0,0)
+  const int cx = threadIdx.x % NTX, cy = threadIdx.x / NTX;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // tile + TT halos, periodic indices straight from the interior (the host
+  // guarantees a tile plus TT halos fits in the interior: one wrap suffices)
+  {
+    // all of this thread's loads in flight before the first shared store
+    constexpr int NLD = (WI * HI + NTX * NTY - 1) / (NTX * NTY);
+    T v[NLD];
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int p = threadIdx.x + k * NTX * NTY;
+      if (p < WI * HI) {
+        const int bx = p % WI, by = p / WI;
+        int x = x0 + bx, y = y0 + by;
+        x += x < 0 ? m0 : (x >= m0 ? -m0 : 0);
+        y += y < 0 ? m1 : (y >= m1 ? -m1 : 0);
+        v[k] = __ldg(a.in + a.org + x + (lope_i64)y * a.s1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int p = threadIdx.x + k * NTX * NTY;
+      if (p < WI * HI) b0[p] = v[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 1; s < TT; ++s) {
+    const T* src = (s & 1) ? b0 : b1;
+    T* dst = (s & 1) ? b1 : b0;
+    for (int by = s * FN1 + cy; by < HI - s * FP1; by += NTY)
+      for (int bx = s * FN0 + cx; bx < WI - s * FP0; bx += NTX) {
+        LopeSmemTile2<T, WI> rd;
+        rd.buf = src;
+        rd.bx = bx;
+        rd.by = by;
+        T res[1];
+        bool slow = false;
+        Body::template eval<T, false>(rd, sc.v, res, slow);
+        dst[by * WI + bx] = res[0];
+      }
+    __syncthreads();
+  }
+  // last step: the tile itself, stored with its periodic images
+  const T* src = (TT & 1) ? b0 : b1;
+  const bool wx = g.wrap & 1, wy = (g.wrap >> 1) & 1;
+  for (int by = TT * FN1 + cy; by < TT * FN1 + TY; by += NTY) {
+    const int y = y0 + by;
+    if (y >= m1) break;
+    const bool yh = wy && y < g.hi[1], yl = wy && y >= m1 - g.lo[1];
+    const lope_i64 yimg = (yh ? (lope_i64)m1 : -(lope_i64)m1) * a.s1;
+    T* orow = a.out + a.org + (lope_i64)y * a.s1;
+    for (int bx = TT * FN0 + cx; bx < TT * FN0 + TX; bx += NTX) {
+      const int x = x0 + bx;
+      if (x >= m0) break;
+      LopeSmemTile2<T, WI> rd;
+      rd.buf = src;
+      rd.bx = bx;
+      rd.by = by;
+      T res[1];
+      bool slow = false;
+      Body::template eval<T, false>(rd, sc.v, res, slow);
+      orow[x] = res[0];
+      const bool xh = wx && x < g.hi[0], xl = wx && x >= m0 - g.lo[0];
+      if (xh | xl | yh | yl) {
+        const int ximg = xh ? m0 : -m0;
+        if (xh | xl) orow[x + ximg] = res[0];
+        if (yh | yl) {
+          orow[x + yimg] = res[0];
+          if (xh | xl) orow[x + ximg + yimg] = res[0];
+        }
+      }
+    }
+  }
+}

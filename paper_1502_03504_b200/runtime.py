@@ -172,6 +172,7 @@ class HaloArray:
         return int(np.prod(self.interior)) * int(self.layout.elem_bytes)
 
 
+_L2_RESIDENT_BYTES = 64 << 20      # fields this small are launch-bound, not HBM-bound
 _AUTOTUNE_MIN_CELLS = 1 << 25      # ~128 MB fp32: below this the defaults are within noise
 
 
@@ -392,13 +393,34 @@ def step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Option
         tuner.after(stream)
 
 
+def multi_step(kernel: CompiledKernel, arr: HaloArray, nsteps: int, scalars=None, stream=None) -> None:
+    """``nsteps`` fused steps (every dim periodic) in as few launches as the kernel
+    allows: rank-2 kernels on fields of at least a tile plus four halos advance four
+    steps per launch in shared memory (``lope_step_multi``), bit-identical to
+    ``nsteps`` calls of ``step``."""
+    if nsteps <= 0:
+        return
+    rs, is_ = kernel.scalar_args(scalars)
+    live = ctypes.c_int32()
+    a, b = arr.data, arr.spare()
+    _lib.check(_lib.lib().lope_step_multi(kernel.handle, ctypes.byref(arr.layout), ctypes.c_void_p(a.data_ptr()),
+                                          ctypes.c_void_p(b.data_ptr()), int(nsteps), rs, is_,
+                                          ctypes.c_void_p(_stream_handle(stream)), ctypes.byref(live)),
+               "lope_step_multi")
+    if live.value == 1:
+        arr.swap()
+
+
 def iterate(kernel: CompiledKernel, arr: HaloArray, steps: int, scalars=None, stream=None) -> None:
     """``do it = 1, steps; HALO_TRANSFER(U); do concurrent (full interior) call K(U); end do``."""
     if steps <= 0:
         return
     halo_transfer(arr, stream=stream)
-    for _ in range(steps - 1):
-        step(kernel, arr, scalars, stream=stream)
+    if arr.layout.count * arr.layout.elem_bytes <= _L2_RESIDENT_BYTES:
+        multi_step(kernel, arr, steps - 1, scalars, stream=stream)   # launch-bound: temporal blocking
+    else:
+        for _ in range(steps - 1):
+            step(kernel, arr, scalars, stream=stream)
     launch(kernel, [arr], None, scalars, stream=stream)
 
 
@@ -441,23 +463,31 @@ class StepGraph:
     ``steps`` should be even so the live buffer is the same after every replay.
     """
 
-    def __init__(self, kernel: CompiledKernel, arr: HaloArray, steps: int, scalars=None):
+    def __init__(self, kernel: CompiledKernel, arr: HaloArray, steps: int, scalars=None, multi: bool = True):
         torch = _torch()
         if steps <= 0:
             raise ValueError("capture a positive number of steps")
         self.arr = arr
         self.steps = steps
+        self.multi = multi                # temporal blocking where the kernel allows it
         arr.spare()                       # both ping-pong buffers exist before capture
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):        # warm the module / tensor-map caches off-graph
+            if multi:
+                multi_step(kernel, arr, 4, scalars, stream=s)
             step(kernel, arr, scalars, stream=s)
             step(kernel, arr, scalars, stream=s)
         torch.cuda.current_stream().wait_stream(s)
         self.graph = torch.cuda.CUDAGraph()
+        l0 = _lib.launch_count()
         with torch.cuda.graph(self.graph):
-            for _ in range(steps):
-                step(kernel, arr, scalars)
+            if multi:
+                multi_step(kernel, arr, steps, scalars)
+            else:
+                for _ in range(steps):
+                    step(kernel, arr, scalars)
+        self.launches = _lib.launch_count() - l0     # kernels per replay
         # capture recorded the launches without running them; the host-side live buffer
         # flipped `steps` times, which is where the data is after one replay (repeated
         # replays with an odd `steps` re-read the captured input buffer)

@@ -301,3 +301,50 @@ def test_plan_tuning_is_bitwise_transparent(name, shape, dt):
     R.launch(k, [arr])
     plain = gpu_iterate(kir, field, n_tune + 2, {}, dt).get_interior()
     assert O.equal_bits(arr.get_interior(), plain)
+
+
+@pytest.mark.parametrize("name,shape,dt,n", [("heat2d", (1024, 1024), "float32", 13),
+                                             ("heat2d", (300, 170), "float64", 9),
+                                             ("box5x5", (256, 192), "float64", 8),
+                                             ("drift2", (200, 160), "float32", 7),
+                                             ("ninept2d", (136, 40), "float32", 5)])
+def test_temporal_blocking_is_bitwise_identical(monkeypatch, name, shape, dt, n):
+    """multi_step (4 steps per launch in shared memory for rank 2) leaves the same
+    padded block -- interior and periodic halo images -- as n single fused steps."""
+    kir = stencils.by_name(name)
+    npdt = np.float32 if dt == "float32" else np.float64
+    sc = {"c": 0.25} if name == "drift2" else None
+    field = O.hash_field(shape, 29, npdt)
+    l_, h_ = halos_of(kir)
+    k = K(kir, dt)
+    a = R.HaloArray(shape, l_, h_, dt)
+    a.set_interior(field)
+    R.halo_transfer(a)
+    R.multi_step(k, a, n, sc)
+    b = R.HaloArray(shape, l_, h_, dt)
+    b.set_interior(field)
+    R.halo_transfer(b)
+    for _ in range(n):
+        R.step(k, b, sc)
+    assert O.equal_bits(a.get_padded(), b.get_padded()), O.first_mismatch(a.get_padded(), b.get_padded())
+    want = field
+    for _ in range(n):
+        want = O.periodic_apply(want, kir, sc, npdt)
+    assert O.equal_bits(a.get_interior(), want)
+
+
+def test_step_graph_with_temporal_blocking_matches_single_steps():
+    kir = stencils.heat2d()
+    field = O.hash_field((512, 256), 31, np.float32)
+    k = K(kir, "float32")
+    a = R.HaloArray(field.shape, [1, 1], [1, 1], "float32")
+    a.set_interior(field)
+    R.halo_transfer(a)
+    g = R.StepGraph(k, a, 10)          # warm-up inside advances the field by 6 steps
+    g.replay()
+    torch.cuda.synchronize()
+    assert g.launches < 10
+    want = field
+    for _ in range(16):
+        want = O.periodic_apply(want, kir, None, np.float32)
+    assert O.equal_bits(a.get_interior(), want)

@@ -10,7 +10,23 @@ a = R.HaloArray(shape, [1, 1], [1, 1], "float32")
 a.fill_hash(1)
 R.halo_transfer(a)
 n = 100
-g = R.StepGraph(k, a, n)
+if os.environ.get("MULTI") == "1":
+    class _G:
+        steps = n
+        def __init__(self):
+            torch.cuda.synchronize()
+            s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                R.multi_step(k, a, n)
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                R.multi_step(k, a, n)
+        def replay(self):
+            self.graph.replay()
+    g = _G()
+else:
+    g = R.StepGraph(k, a, n)
 g.replay(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
