@@ -459,7 +459,14 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.pw << ">(&map, a, sc, g);\n}\n";
   }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1) {
-    const int tx = K->dtype == LOPE_F32 ? 128 : 64, ty = 32, tt = 4;
+    // 128 x 28 fp32 tiles: 1024^2 splits into 296 = 2 x 148 CTAs (config 1, measured
+    // 2.27 us/step vs 2.47 at 32 rows); 8 steps per launch for one-cell footprints,
+    // 4 for wider ones (the recomputed halo grows with the footprint)
+    const int tx = K->dtype == LOPE_F32 ? 128 : 64;
+    const int wmax = std::max(k.fn[0][0] + k.fp[0][0], k.fn[0][1] + k.fp[0][1]);
+    int ty = 28, tt = wmax <= 2 ? 8 : 4;
+    if (const char* e = std::getenv("LOPE_TBLOCK_TY")) ty = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LOPE_TBLOCK_TT")) tt = std::max(1, std::atoi(e));
     s << "typedef LopeTblockCfg<LopeBody, LT, " << tx << ", " << ty << ", " << tt << "> LopeTbCfg;\n";
     s << "extern \"C\" __constant__ int lope_tblock_info[4] = {LopeTbCfg::SMEM_BYTES, " << tx << ", " << ty << ", "
       << tt << "};\n";

@@ -820,25 +820,33 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
   // tile + TT halos, periodic indices straight from the interior (the host
   // guarantees a tile plus TT halos fits in the interior: one wrap suffices)
   {
-    // all of this thread's loads in flight before the first shared store
-    constexpr int NLD = (WI * HI + NTX * NTY - 1) / (NTX * NTY);
-    T v[NLD];
+    // all of this thread's loads in flight before the first shared store: columns
+    // cx, cx + NTX (wrapped once), rows cy, cy + NTY, ... (wrapped per row)
+    constexpr int NCOL = (WI + NTX - 1) / NTX, NROW = (HI + NTY - 1) / NTY;
+    int xw[NCOL];
 #pragma unroll
-    for (int k = 0; k < NLD; ++k) {
-      const int p = threadIdx.x + k * NTX * NTY;
-      if (p < WI * HI) {
-        const int bx = p % WI, by = p / WI;
-        int x = x0 + bx, y = y0 + by;
-        x += x < 0 ? m0 : (x >= m0 ? -m0 : 0);
-        y += y < 0 ? m1 : (y >= m1 ? -m1 : 0);
-        v[k] = __ldg(a.in + a.org + x + (lope_i64)y * a.s1);
+    for (int c = 0; c < NCOL; ++c) {
+      int x = x0 + cx + c * NTX;
+      xw[c] = x + (x < 0 ? m0 : (x >= m0 ? -m0 : 0));
+    }
+    T v[NROW][NCOL];
+#pragma unroll
+    for (int r = 0; r < NROW; ++r) {
+      const int by = cy + r * NTY;
+      int y = y0 + by;
+      y += y < 0 ? m1 : (y >= m1 ? -m1 : 0);
+      const T* row = a.in + a.org + (lope_i64)y * a.s1;
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c)
+        if (by < HI && cx + c * NTX < WI) v[r][c] = __ldg(row + xw[c]);
+    }
+#pragma unroll
+    for (int r = 0; r < NROW; ++r)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) {
+        const int by = cy + r * NTY, bx = cx + c * NTX;
+        if (by < HI && bx < WI) b0[by * WI + bx] = v[r][c];
       }
-    }
-#pragma unroll
-    for (int k = 0; k < NLD; ++k) {
-      const int p = threadIdx.x + k * NTX * NTY;
-      if (p < WI * HI) b0[p] = v[k];
-    }
   }
   __syncthreads();
 #pragma unroll

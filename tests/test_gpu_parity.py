@@ -303,11 +303,13 @@ def test_plan_tuning_is_bitwise_transparent(name, shape, dt):
     assert O.equal_bits(arr.get_interior(), plain)
 
 
-@pytest.mark.parametrize("name,shape,dt,n", [("heat2d", (1024, 1024), "float32", 13),
-                                             ("heat2d", (300, 170), "float64", 9),
+@pytest.mark.parametrize("name,shape,dt,n", [("heat2d", (1024, 1024), "float32", 17),
+                                             ("heat2d", (300, 170), "float64", 17),
                                              ("box5x5", (256, 192), "float64", 8),
-                                             ("drift2", (200, 160), "float32", 7),
-                                             ("ninept2d", (136, 40), "float32", 5)])
+                                             ("drift2", (200, 160), "float32", 16),
+                                             ("ninept2d", (144, 44), "float32", 17),
+                                             ("box5x5", (160, 64), "float32", 12),
+                                             ("heat2d", (100, 60), "float32", 6)])
 def test_temporal_blocking_is_bitwise_identical(monkeypatch, name, shape, dt, n):
     """multi_step (4 steps per launch in shared memory for rank 2) leaves the same
     padded block -- interior and periodic halo images -- as n single fused steps."""
@@ -340,11 +342,11 @@ def test_step_graph_with_temporal_blocking_matches_single_steps():
     a = R.HaloArray(field.shape, [1, 1], [1, 1], "float32")
     a.set_interior(field)
     R.halo_transfer(a)
-    g = R.StepGraph(k, a, 10)          # warm-up inside advances the field by 6 steps
+    g = R.StepGraph(k, a, 16)          # warm-up inside advances the field by 6 steps
     g.replay()
     torch.cuda.synchronize()
-    assert g.launches < 10
+    assert g.launches < 16
     want = field
-    for _ in range(16):
+    for _ in range(22):
         want = O.periodic_apply(want, kir, None, np.float32)
     assert O.equal_bits(a.get_interior(), want)
