@@ -249,6 +249,7 @@ def run_gpu_arm(args, wl):
         group = dist.group.WORLD
     kir = stencils.by_name(wl["kernel"])
     kern = R.CompiledKernel(kir, wl["dtype"])
+    exchange_kind = None
     fp = kir.footprints[kir.array_params[0]].dims
     lo, hi = [n for n, _ in fp], [p for _, p in fp]
     shape = tuple(wl["shape"])
@@ -262,7 +263,18 @@ def run_gpu_arm(args, wl):
         gext = list(shape[:-1]) + [shape[-1] * ws]
         gorg = [0] * (len(shape) - 1) + [shape[-1] * rank]
         field.block.fill_hash(SEED, gext, gorg)
-        stepper = D.SlabStepper(kern, field)
+        # fused exchange: the kernel stores boundary planes into the neighbours' halos
+        # through CUDA IPC peer memory; NCCL send/recv overlapped with the interior if
+        # the peer mapping is unavailable
+        exchange_kind = "fused-peer-store"
+        try:
+            if os.environ.get("LOPE_EXCHANGE", "peer") != "peer":
+                raise RuntimeError("LOPE_EXCHANGE selects NCCL")
+            stepper = D.PeerSlabStepper(kern, field, group=group)
+        except Exception as e:             # pragma: no cover - depends on the node
+            log("peer exchange unavailable, using NCCL send/recv:", e)
+            exchange_kind = "nccl-send-recv-overlapped"
+            stepper = D.SlabStepper(kern, field)
         stepper.exchange()
 
         def do_step():
@@ -373,6 +385,7 @@ def run_gpu_arm(args, wl):
             "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
                        "shape_per_gpu": list(shape), "global_shape": list(shape[:-1]) + [shape[-1] * ws],
                        "halo": [lo, hi], "parallelism": f"slab{ws}" if ws > 1 else "single",
+                       "exchange": exchange_kind if ws > 1 else "in-kernel periodic images",
                        "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
                              else "L2-resident working set (config 1); HBM fraction informational",
                        "hbm_gbs_alg": round(alg_bytes * ws / (ms_per_step / 1e3) / 1e9 / ws, 1)},

@@ -140,6 +140,27 @@ int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const i
 int lope_step_multi(const lope_kernel* k, const lope_layout* layout, void* buf0, void* buf1, int64_t nsteps,
                     const double* rscal, const int64_t* iscal, void* stream, int32_t* live_index);
 
+/* lope_step_planes whose periodic images along the slowest dim are stored straight
+ * into the neighbours' output blocks (same layout): the first `hi` planes' images into
+ * `lo_peer_out` (the low neighbour's high halo), the last `lo` planes' into
+ * `hi_peer_out` (the high neighbour's low halo); NULL = this block.  With the
+ * neighbours' buffers mapped through CUDA IPC (NVLink peer memory) the halo exchange
+ * is fused into the stencil kernel: no exchange kernel or copy; the caller orders
+ * steps with a barrier.  Replaces the face fills of runtime.py:688-697. */
+int lope_step_planes_peer(const lope_kernel* k, const lope_layout* layout, const void* in, void* out,
+                          int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
+                          int32_t wrap_mask, const void* lo_peer_out, const void* hi_peer_out, void* stream);
+
+/* Device-to-device byte copy on `stream` (peer pointers included): the initial face
+ * fill of the fused-exchange slabs. */
+int lope_copy_bytes(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* CUDA IPC for the peer blocks: export a device pointer (64-byte handle + offset
+ * into its allocation), open it in another process, close it. */
+int lope_ipc_export(const void* ptr, uint8_t* handle, int64_t* offset);
+int lope_ipc_open(const uint8_t* handle, int64_t offset, void** ptr);
+int lope_ipc_close(void* ptr);
+
 /* Execution plans (which compiled tile variant, which z-chunk) for the tiled kernel.
  * lope_plan_candidates compiles the candidate variants and lists (variant, z-chunk,
  * y-band of the unit walk) triples (n = how many exist; at most `cap` are written).  lope_plan_set makes one of

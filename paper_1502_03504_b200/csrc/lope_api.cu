@@ -74,6 +74,7 @@ struct Drv {
   decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
   decltype(&cuLaunchKernel) launchKernel = nullptr;
   decltype(&cuLaunchKernelEx) launchKernelEx = nullptr;   // optional (PDL launches)
+  decltype(&cuMemGetAddressRange) memGetAddressRange = nullptr;   // optional (IPC export)
   decltype(&cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
   decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
   decltype(&cuGetErrorString) getErrorString = nullptr;
@@ -105,6 +106,7 @@ Drv& drv() {
   if (d.ok) {
     std::string keep = d.why;
     if (!get("cuLaunchKernelEx", (void**)&d.launchKernelEx)) d.launchKernelEx = nullptr;
+    if (!get("cuMemGetAddressRange", (void**)&d.memGetAddressRange)) d.memGetAddressRange = nullptr;
     d.why = keep;
   }
   return d;
@@ -307,6 +309,7 @@ template <class T> struct HScal { T v[LOPE_HOST_MAX_SCAL]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
   int wrap, zchunk, xshift, box0, p1, yband;
+  long long sdl, sdh;
 };
 
 }  // namespace
@@ -445,7 +448,8 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
   s << "struct LopeArrPack { LopeArr<LT> a[" << k.arrays.size() << "]; };\n";
   s << "extern \"C\" __global__ void __launch_bounds__(128) lope_generic("
        "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
-       "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n}\n";
+       "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n"
+       "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   if (V.tiled_ok) {
     const TileCfg& c = V.tile;
     s << "typedef LopeTiledCfg<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
@@ -456,7 +460,8 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.mb << ") lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
-      << ", " << c.pw << ">(&map, a, sc, g);\n}\n";
+      << ", " << c.pw << ">(&map, a, sc, g);\n"
+      << "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1) {
     // 128 x 28 fp32 tiles: 1024^2 splits into 296 = 2 x 148 CTAs (config 1, measured
@@ -745,7 +750,7 @@ std::string plan_key(const lope_layout* L, int wrap) {
 template <class T>
 int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const int ext[3],
              const void* const* in, void* const* out, const double* rs, const int64_t* is, int wrap,
-             cudaStream_t st, int vi = -1, int zc = 0, int yband = 0) {
+             cudaStream_t st, int vi = -1, int zc = 0, int yband = 0, long long sdl = 0, long long sdh = 0) {
   if (vi < 0) {
     vi = 0;
     if (!K->plans.empty()) {
@@ -774,6 +779,8 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   g.wrap = wrap;
   g.zchunk = zc > 0 ? zc : zchunk_default(k);
   g.yband = yband;
+  g.sdl = sdl;
+  g.sdh = sdh;
   if (const char* e = std::getenv("LOPE_YBAND")) g.yband = std::atoi(e);
   const int vx = 16 / (int)sizeof(T);
   {
@@ -1114,9 +1121,12 @@ int lope_step(const lope_kernel* kc, const lope_layout* layout, const void* in, 
                           wrap_mask, stream);
 }
 
-int lope_step_planes(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
-                     int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
-                     int32_t wrap_mask, void* stream) {
+}  // extern "C"
+
+namespace {
+int step_planes_impl(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out, int64_t begin,
+                     int64_t end, const double* rscal, const int64_t* iscal, int32_t wrap_mask,
+                     const void* lo_peer, const void* hi_peer, void* stream) {
   lope_kernel* k = const_cast<lope_kernel*>(kc);
   if (!k || !layout) return fail(108, "null argument");
   if (int e = check_layout(layout)) return e;
@@ -1143,8 +1153,35 @@ int lope_step_planes(const lope_kernel* kc, const lope_layout* layout, const voi
   void* outs[1] = {out};
   int wrap = wrap_mask & ((1 << ir.rank) - 1);
   cudaStream_t st = (cudaStream_t)stream;
-  return k->dtype == LOPE_F32 ? run_body<float>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st)
-                              : run_body<double>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st);
+  long long sdl = 0, sdh = 0;
+  if (lo_peer || hi_peer) {
+    if (!((wrap >> sd) & 1)) return fail(108, "peer images need the slowest dim in the wrap mask");
+    const long long eb = (long long)layout->elem_bytes;
+    const long long dl = lo_peer ? (long long)((const char*)lo_peer - (const char*)out) : 0;
+    const long long dh = hi_peer ? (long long)((const char*)hi_peer - (const char*)out) : 0;
+    if (dl % eb || dh % eb) return fail(108, "peer buffers are not element-aligned with the output");
+    sdl = dl / eb;
+    sdh = dh / eb;
+  }
+  return k->dtype == LOPE_F32
+             ? run_body<float>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st, -1, 0, 0, sdl, sdh)
+             : run_body<double>(k, layout, r0, ext, ins, outs, rscal, iscal, wrap, st, -1, 0, 0, sdl, sdh);
+}
+}  // namespace
+
+extern "C" {
+
+int lope_step_planes(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
+                     int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
+                     int32_t wrap_mask, void* stream) {
+  return step_planes_impl(kc, layout, in, out, begin, end, rscal, iscal, wrap_mask, nullptr, nullptr, stream);
+}
+
+int lope_step_planes_peer(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
+                          int64_t begin, int64_t end, const double* rscal, const int64_t* iscal,
+                          int32_t wrap_mask, const void* lo_peer_out, const void* hi_peer_out, void* stream) {
+  return step_planes_impl(kc, layout, in, out, begin, end, rscal, iscal, wrap_mask, lo_peer_out, hi_peer_out,
+                          stream);
 }
 
 }  // extern "C"
@@ -1267,6 +1304,62 @@ int lope_step_multi(const lope_kernel* kc, const lope_layout* layout, void* buf0
   }
   (void)d;
   *live_index = live;
+  return 0;
+}
+
+int lope_copy_bytes(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0) return fail(108, "negative byte count");
+  if (bytes == 0) return 0;
+  if (!dst || !src) return fail(202, "null buffer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
+// ---- CUDA IPC: the neighbours' output blocks for fused peer-store exchange ----
+
+namespace {
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_bases;   // opened pointer -> mapping base
+}
+
+int lope_ipc_export(const void* ptr, uint8_t* handle, int64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(108, "null argument");
+  Drv& d = drv();
+  if (!d.ok || !d.memGetAddressRange) return fail(-3, "cuMemGetAddressRange unavailable");
+  CUDA_TRY(cudaFree(nullptr));
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = d.memGetAddressRange(&base, &size, (CUdeviceptr)ptr);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMemGetAddressRange");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  std::memcpy(handle, &h, sizeof h);
+  *offset = (int64_t)((CUdeviceptr)ptr - base);
+  return 0;
+}
+
+int lope_ipc_open(const uint8_t* handle, int64_t offset, void** ptr) {
+  if (!handle || !ptr) return fail(108, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr = (char*)base + offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_bases[*ptr] = base;
+  return 0;
+}
+
+int lope_ipc_close(void* ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_bases.find(ptr);
+    if (it == g_ipc_bases.end()) return fail(108, "pointer was not opened by lope_ipc_open");
+    base = it->second;
+    g_ipc_bases.erase(it);
+  }
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
   return 0;
 }
 

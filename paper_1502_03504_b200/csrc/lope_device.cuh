@@ -167,6 +167,11 @@ struct LopeGeom {
   int box0;       // tiled: TMA x coordinate of tile 0's box (row-relative, already shifted)
   int p1;         // tiled: padded rows per plane; > 0 selects the flattened 2-D tensor map
   int yband;      // tiled: tile rows per band of the unit walk (0: whole plane)
+  // Fused exchange: periodic images along the slowest dim go to another buffer --
+  // the low / high neighbour's output block (NVLink peer memory under CUDA IPC) --
+  // at this element offset from `out` (0: the image lives in this block's halo).
+  lope_i64 sdl;   // images of the first `hi` planes (into the low neighbour's high halo)
+  lope_i64 sdh;   // images of the last `lo` planes (into the high neighbour's low halo)
 };
 
 // --------------------------------------------------------------------------
@@ -175,7 +180,7 @@ struct LopeGeom {
 template <class T>
 __device__ __noinline__ void lope_store_images(T* __restrict__ out, lope_i64 s1, lope_i64 s2,
                                                   lope_i64 org0, int x, int y, int z,
-                                                  const LopeGeom& g, T v) {
+                                                  const LopeGeom& g, T v, int rank = 3) {
   // (x,y,z) are 0-based interior coordinates; org0 = flat offset of interior (0,0,0).
   // Per dim: the point itself, its image in the high halo (x < hi -> x+m) and its
   // image in the low halo (x >= m-lo -> x-m).  Written without arrays so the
@@ -197,7 +202,10 @@ __device__ __noinline__ void lope_store_images(T* __restrict__ out, lope_i64 s1,
         if ((a | b | c) == 0) continue;
         const bool cx = a == 0 ? true : (a == 1 ? xh : xl);
         const int xx = a == 0 ? x : (a == 1 ? x + g.m[0] : x - g.m[0]);
-        if (cx && cy && cz) out[org0 + (lope_i64)xx + (lope_i64)yy * s1 + (lope_i64)zz * s2] = v;
+        // slowest-dim images may belong to a neighbour's block (g.sdl / g.sdh)
+        const int sc = rank == 3 ? c : (rank == 2 ? b : a);
+        const lope_i64 dl = sc == 0 ? 0 : (sc == 1 ? g.sdl : g.sdh);
+        if (cx && cy && cz) out[org0 + dl + (lope_i64)xx + (lope_i64)yy * s1 + (lope_i64)zz * s2] = v;
       }
     }
   }
@@ -249,7 +257,7 @@ __device__ __forceinline__ void lope_generic_impl(const LopeArr<T>* arrs, const 
           const lope_i64 org0 = arrs[A].org - g.r0[0] - (lope_i64)g.r0[1] * arrs[A].s1 -
                                 (lope_i64)g.r0[2] * arrs[A].s2;
           lope_store_images<T>(o, arrs[A].s1, arrs[A].s2, org0, i + g.r0[0], j + g.r0[1],
-                               k + g.r0[2], g, res[q]);
+                               k + g.r0[2], g, res[q], Body::RANK);
         }
       }
     }
@@ -742,7 +750,8 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           if (wx_any && xw) *reinterpret_cast<V*>(orow + (lope_i64)r * s1 + ximg) = o;
         }
       } else {
-        const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] : -(lope_i64)g.m[2]) * s2;
+        // z images (rank 3: the slowest dim, possibly in a neighbour's block)
+        const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
           if (r >= nrow) continue;
@@ -756,7 +765,9 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           const int yg = ybase + r + g.r0[1];
           const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
           if (yw | zw) {
-            const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] : -(lope_i64)g.m[1]) * s1;
+            // y images (rank 2: the slowest dim, possibly in a neighbour's block)
+            const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdl : 0)
+                                                : -(lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdh : 0));
             if (yw) {
               *reinterpret_cast<V*>(p + yimg) = o;
               if (xw) *reinterpret_cast<V*>(p + yimg + ximg) = o;

@@ -351,11 +351,21 @@ class MultiSlab:
 def run_pinned(kernel, local_shape, lo, hi, dtype, host_in, host_out, steps, group=None, scalars=None):
     """End-to-end on this rank's slab: pinned host slab in, ``steps`` iterations, host slab out."""
     import torch
+    import os
     arr = SlabArray(local_shape, lo, hi, dtype, group=group)
     arr.block.upload(host_in.data_ptr())
-    SlabStepper(kernel, arr, scalars).iterate(steps)
+    st = None
+    if arr.size > 1 and os.environ.get("LOPE_EXCHANGE", "peer") == "peer":
+        try:
+            st = PeerSlabStepper(kernel, arr, scalars, group=group)
+        except Exception:          # pragma: no cover - peer mapping unavailable on this node
+            st = None
+    (st or SlabStepper(kernel, arr, scalars)).iterate(steps)
     arr.block.download(host_out.data_ptr())
     torch.cuda.current_stream().synchronize()
+    if st is not None:
+        st.barrier()
+        st.close()
 
 
 # ---------------------------------------------------------------------------
@@ -661,3 +671,212 @@ class MultiGrid:
             self.step()
         for b in self.blocks:
             launch(self.kernel, [b], None, self.scalars)
+
+
+# ---------------------------------------------------------------------------
+# Fused exchange: the stencil kernel stores boundary planes into the neighbours'
+# halos through NVLink peer memory (lope_step_planes_peer + CUDA IPC)
+
+
+def _step_planes_peer(kernel, layout, src, dst, b, e, rs, is_, mask, lo_peer, hi_peer, stream):
+    _lib.check(_lib.lib().lope_step_planes_peer(kernel.handle, ctypes.byref(layout), ctypes.c_void_p(src),
+                                                ctypes.c_void_p(dst), b, e, rs, is_, mask,
+                                                ctypes.c_void_p(lo_peer), ctypes.c_void_p(hi_peer),
+                                                _stream_ptr(stream)), "lope_step_planes_peer")
+
+
+class PeerMultiSlab:
+    """P slabs on one GPU with the fused exchange: each block's kernel stores its
+    boundary planes' images straight into the neighbouring blocks' halos, so a step
+    is P kernels and no exchange at all.  Checks the peer-store epilogue against the
+    undecomposed run (the multi-GPU version maps the neighbours through CUDA IPC)."""
+
+    def __init__(self, kernel, global_shape, lo, hi, dtype, nranks: int, scalars=None):
+        from .runtime import HaloArray
+        self.grid = SlabGrid(global_shape, nranks, lo, hi)
+        self.kernel = kernel
+        self.scalars = scalars
+        self.blocks = [HaloArray(self.grid.local_shape, lo, hi, dtype) for _ in range(nranks)]
+        for b in self.blocks:
+            b.spare()
+        self.dim = len(global_shape) - 1
+        self._rs, self._is = kernel.scalar_args(scalars)
+
+    set_global = MultiSlab.set_global
+    get_global = MultiSlab.get_global
+    _mask = MultiSlab._mask
+    halo_transfer = MultiSlab.halo_transfer
+
+    def step(self) -> None:
+        P = len(self.blocks)
+        L = self.blocks[0].layout
+        m = int(L.interior[self.dim])
+        full = (1 << len(self.grid.global_shape)) - 1
+        outs = [b.spare().data_ptr() for b in self.blocks]
+        for r, b in enumerate(self.blocks):
+            lo_peer = outs[(r - 1) % P] if P > 1 else 0
+            hi_peer = outs[(r + 1) % P] if P > 1 else 0
+            _step_planes_peer(self.kernel, b.layout, b.data.data_ptr(), outs[r], 0, m, self._rs, self._is,
+                              full, lo_peer, hi_peer, None)
+        for b in self.blocks:
+            b.swap()
+
+    def iterate(self, steps: int) -> None:
+        from .runtime import launch
+        if steps <= 0:
+            return
+        self.halo_transfer()
+        for _ in range(steps - 1):
+            self.step()
+        for b in self.blocks:
+            launch(self.kernel, [b], None, self.scalars)
+
+
+class PeerSlabStepper:
+    """Multi-GPU slabs with the exchange fused into the kernel (one process per GPU).
+
+    At setup every rank exports both ping-pong buffers of its block (CUDA IPC) and
+    opens its two ring neighbours'.  A step is one kernel per rank that writes its
+    interior, the periodic images of the non-decomposed dims, and its boundary
+    planes' images directly into the neighbours' output blocks over NVLink; a
+    barrier then orders the step against the next one (the neighbours' halos are
+    complete, and nobody still reads the buffers the next step overwrites).  With
+    NCCL the barrier is a one-element all-reduce on the compute stream; with gloo
+    (tests) a device synchronise plus ``dist.barrier``.
+    """
+
+    def __init__(self, kernel, arr: SlabArray, scalars=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.kernel = kernel
+        self.arr = arr
+        self.scalars = scalars
+        self.group = group
+        self.dist = dist
+        self._rs, self._is = kernel.scalar_args(scalars)
+        blk = arr.block
+        blk.spare()
+        self.rank, self.size = arr.rank, arr.size
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._flag = torch.zeros(1, dtype=torch.int32, device=blk.data.device)
+        mine = []
+        for buf in blk._bufs:
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64()
+            _lib.check(_lib.lib().lope_ipc_export(ctypes.c_void_p(buf.data_ptr()), h, ctypes.byref(off)),
+                       "lope_ipc_export")
+            mine.append((bytes(h.raw), int(off.value)))
+        allh = [None] * self.size
+        dist.all_gather_object(allh, mine, group=group)
+        prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
+        self._opened = []
+        self.peers = {}
+        for who in sorted({prev, nxt}):
+            ptrs = []
+            for (h, off) in allh[who]:
+                if who == self.rank:
+                    ptrs = [b.data_ptr() for b in blk._bufs]
+                    break
+                p = ctypes.c_void_p()
+                _lib.check(_lib.lib().lope_ipc_open(h, off, ctypes.byref(p)), "lope_ipc_open")
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+            self.peers[who] = ptrs
+        self.prev, self.next = prev, nxt
+        d = arr.dim
+        L = blk.layout
+        self.m = int(L.interior[d])
+        self.full = (1 << blk.rank) - 1
+
+    def close(self) -> None:
+        for p in self._opened:
+            _lib.lib().lope_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+
+    def barrier(self) -> None:
+        import torch
+        if self._nccl:
+            self.dist.all_reduce(self._flag, group=self.group)     # stream-ordered
+        else:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+
+    def exchange(self) -> None:
+        """``HALO_TRANSFER``: local dims wrap on the GPU, the decomposed dim's halo
+        planes are copied from the neighbours' live blocks through peer memory."""
+        from .runtime import halo_transfer
+        blk = self.arr.block
+        if self.size == 1:
+            halo_transfer(blk)
+            return
+        halo_transfer(blk, dims_mask=self.arr.local_mask)
+        self.barrier()
+        live = blk._live
+        eb = int(blk.layout.elem_bytes)
+        spans = {w: _lib.face_span(blk.layout, w) for w in range(4)}
+        base = blk.data.data_ptr()
+        # low halo <- previous image's last `lo` planes; high halo <- next image's first `hi`
+        for dst_w, who, src_w in ((0, self.prev, 3), (1, self.next, 2)):
+            off, cnt = spans[dst_w]
+            soff, _ = spans[src_w]
+            if cnt:
+                _lib.check(_lib.lib().lope_copy_bytes(ctypes.c_void_p(base + off * eb),
+                                                      ctypes.c_void_p(self.peers[who][live] + soff * eb),
+                                                      cnt * eb, _stream_ptr(None)), "lope_copy_bytes")
+        self.barrier()
+
+    def tune(self) -> int:
+        """Run real steps until the plan for this block is chosen; returns the count."""
+        n = 0
+        while self.kernel.tuner(self.arr.block, self.full) is not None:
+            self.step()
+            n += 1
+        return n
+
+    def kernel_ms_estimate(self, reps: int = 5) -> float:
+        """Average device time of the fused kernel over the whole slab (no barrier)."""
+        import torch
+        blk = self.arr.block
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        out = 1 - blk._live
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            _step_planes_peer(self.kernel, blk.layout, blk.data.data_ptr(), blk.spare().data_ptr(), 0, self.m,
+                              self._rs, self._is, self.full, self.peers[self.prev][out] if self.size > 1 else 0,
+                              self.peers[self.next][out] if self.size > 1 else 0, None)
+        e1.record()
+        torch.cuda.synchronize()
+        self.barrier()
+        return e0.elapsed_time(e1) / reps
+
+    def step(self) -> None:
+        blk = self.arr.block
+        if self.size == 1:
+            from .runtime import step
+            step(self.kernel, blk, self.scalars)
+            return
+        tuner = self.kernel.tuner(blk, self.full)
+        if tuner is not None:
+            tuner.before()
+        self._step()
+        if tuner is not None:
+            tuner.after()
+
+    def _step(self) -> None:
+        blk = self.arr.block
+        out = 1 - blk._live
+        _step_planes_peer(self.kernel, blk.layout, blk.data.data_ptr(), blk.spare().data_ptr(), 0, self.m,
+                          self._rs, self._is, self.full, self.peers[self.prev][out], self.peers[self.next][out],
+                          None)
+        blk.swap()
+        self.barrier()
+
+    def iterate(self, steps: int) -> None:
+        from .runtime import launch
+        if steps <= 0:
+            return
+        self.exchange()
+        for _ in range(steps - 1):
+            self.step()
+        launch(self.kernel, [self.arr.block], None, self.scalars)

@@ -133,3 +133,81 @@ def test_box_pack_unpack_round_trip(dt):
         ref[b[0]:b[0] + e[0], b[1]:b[1] + e[1], b[2]:b[2] + e[2]] = padded[b[0]:b[0] + e[0], b[1]:b[1] + e[1],
                                                                            b[2]:b[2] + e[2]]
         assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,shape,dt,ps", [
+    ("lap3d7", (64, 40, 48), "float32", (1, 2, 3, 4)),
+    ("box5x5", (96, 64), "float64", (2, 4)),
+    ("heat2d", (256, 96), "float64", (3,)),
+    ("drift2", (64, 48), "float32", (2,)),
+])
+def test_fused_peer_exchange_is_bitwise_invariant(name, shape, dt, ps):
+    """Kernels that store their boundary planes into the neighbouring blocks' halos
+    (lope_step_planes_peer) need no exchange step and give the undecomposed bits."""
+    kir = stencils.by_name(name)
+    lo, hi = halos(kir)
+    npdt = np.float32 if dt == "float32" else np.float64
+    sc = {"c": 0.25} if name == "drift2" else None
+    field = O.hash_field(shape, 37, npdt)
+    k = R.CompiledKernel(kir, dt)
+    base = R.HaloArray(shape, lo, hi, dt)
+    base.set_interior(field)
+    R.iterate(k, base, 5, sc)
+    want = base.get_interior()
+    for p in ps:
+        ms = D.PeerMultiSlab(k, shape, lo, hi, dt, p, sc)
+        ms.set_global(field)
+        ms.iterate(5)
+        got = ms.get_global()
+        assert O.equal_bits(got, want), (name, p, O.first_mismatch(got, want))
+
+
+def _peer_worker(rank, size, port, q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        kir = stencils.lap3d7()
+        gshape = (64, 32, 16 * size)
+        field = O.hash_field(gshape, 51, np.float32)
+        k = R.CompiledKernel(kir, "float32")
+        arr = D.SlabArray((64, 32, 16), (1, 1, 1), (1, 1, 1), "float32")
+        arr.block.set_interior(np.ascontiguousarray(field[..., rank * 16:(rank + 1) * 16]))
+        st = D.PeerSlabStepper(k, arr)
+        st.iterate(6)
+        torch.cuda.synchronize()
+        got = arr.block.get_interior()
+        want = field
+        for _ in range(6):
+            want = O.periodic_apply(want, kir, None, np.float32)
+        ok = O.equal_bits(got, want[..., rank * 16:(rank + 1) * 16])
+        dist.barrier()
+        st.close()
+        q.put((rank, bool(ok)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_exchange_across_processes_via_ipc():
+    """Two processes (one GPU here, one per GPU in production) map each other's
+    blocks with CUDA IPC; the fused kernels write across the process boundary."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v is True for v in res.values()), res
