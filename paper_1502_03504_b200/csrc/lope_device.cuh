@@ -318,18 +318,6 @@ __device__ __forceinline__ void lope_tma_load_2d(void* dst, const LopeTmap* map,
       "l"((lope_u64)map), "r"(c0), "r"(c1), "r"(lope_smem_u32(bar))
       : "memory");
 }
-#ifdef LOPE_TMA_EVICT_LAST
-__device__ __forceinline__ void lope_tma_load_2d_hint(void* dst, const LopeTmap* map, lope_u64* bar, int c0,
-                                                      int c1) {
-  lope_u64 pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(lope_smem_u32(dst)),
-      "l"((lope_u64)map), "r"(c0), "r"(c1), "r"(lope_smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-#endif
 __device__ __forceinline__ void lope_tma_prefetch_desc(const LopeTmap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"((lope_u64)map) : "memory");
 }
@@ -349,21 +337,6 @@ template <class T> struct LopeVec;
 template <> struct LopeVec<float> { typedef float4 V; };
 template <> struct LopeVec<double> { typedef double2 V; };
 
-#ifdef LOPE_ST_EVICT_FIRST
-__device__ __forceinline__ void lope_st_evict_first(float* p, float4 v) {
-  lope_u64 pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
-               "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void lope_st_evict_first(double* p, double2 v) {
-  lope_u64 pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
-               : "memory");
-}
-#endif
 
 template <class T, int NR, int NXW, int FZN, int FN0, int FN1, int RY, int VX, bool ZHIST>
 struct LopeWinReader {
@@ -400,11 +373,7 @@ struct LopeTiledCfg {
   static constexpr int BOXX = PADX + BX + ((Body::FP0 + VX - 1) / VX) * VX;
   static constexpr int BOXY = BY + Body::FN1 + Body::FP1;
   static constexpr int NZW = Body::FN2 + Body::FP2 + 1;
-#ifdef LOPE_NO_ZHIST
-  static constexpr bool ZHIST = false;   // experiment: all z planes from the ring
-#else
   static constexpr bool ZHIST = Body::ZSTAR && Body::FN2 > 0;
-#endif
   static constexpr int HOLD = ZHIST ? Body::FP2 + 1 : NZW;     // slots one plane iteration holds
   static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
   static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
@@ -516,14 +485,6 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
   }
   auto produce = [&](lope_u32 limit) {
     while (p_L < limit && p_u < nunits) {
-#ifdef LOPE_STAGGER2
-      // experiment: delay the first load of odd-parity tiles' units
-      if (p_pl == 0 && ((pw.tx + pw.ty()) & 1)) {
-        lope_u64 t0, t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1)); } while (t1 - t0 < (lope_u64)(LOPE_STAGGER2));
-      }
-#endif
       const lope_u32 slot = p_L % NS;
       if (p_L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((p_L / NS) - 1) & 1);
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
@@ -602,25 +563,6 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
         if (ZHIST && k < FZN && pz > 0) continue;          // past planes come from registers
         lope_mbar_wait(&full[L % NS], (L / NS) & 1);
       }
-#ifdef LOPE_DEBUG_NOCOMPUTE
-      __syncwarp();
-      if (lane == 0) {
-        lope_mbar_arrive(&empty[(lbase + pz) % NS]);
-        if (pz == nz - 1)
-          for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
-      }
-      if (xfull && nrow == RY) {
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          V o;
-          T* oe = reinterpret_cast<T*>(&o);
-#pragma unroll
-          for (int e = 0; e < VX; ++e) oe[e] = T(0);
-          *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
-        }
-      }
-      continue;
-#endif
       if (ZHIST && pz == 0) {
         // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
 #pragma unroll
@@ -742,11 +684,7 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
           for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
-#ifdef LOPE_ST_EVICT_FIRST
-          lope_st_evict_first(orow + (lope_i64)r * s1, o);
-#else
           *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
-#endif
           if (wx_any && xw) *reinterpret_cast<V*>(orow + (lope_i64)r * s1 + ximg) = o;
         }
       } else {

@@ -350,3 +350,31 @@ def test_step_graph_with_temporal_blocking_matches_single_steps():
     for _ in range(22):
         want = O.periodic_apply(want, kir, None, np.float32)
     assert O.equal_bits(a.get_interior(), want)
+
+
+def test_full_size_every_plan_family_matches_generic(monkeypatch):
+    """Config 3 at full size: each execution-plan family the tuner can pick (in-band
+    producer with long z-chunks, dedicated producer with short chunks, deeper rings)
+    gives the generic kernel's bits after 3 steps."""
+    monkeypatch.setenv("LOPE_AUTOTUNE", "0")
+    kir = stencils.lap3d7()
+    shape = (1024, 1024, 1024)
+    monkeypatch.setenv("LOPE_FORCE_GENERIC", "1")
+    ref = R.HaloArray(shape, (1, 1, 1), (1, 1, 1), "float32")
+    ref.fill_hash(11)
+    R.iterate(K(kir, "float32"), ref, 3)
+    want = ref.padded_view().contiguous().view(torch.int32).clone()
+    del ref
+    monkeypatch.delenv("LOPE_FORCE_GENERIC")
+    k = R.CompiledKernel(kir, "float32")
+    a = R.HaloArray(shape, (1, 1, 1), (1, 1, 1), "float32")
+    t = R.PlanTuner(k, a.layout, 7)
+    assert len(t.cands) >= 6
+    for cand in t.cands[::4]:
+        t._set(*cand)
+        a.fill_hash(11)
+        R.iterate(k, a, 3)
+        got = a.padded_view().contiguous().view(torch.int32)
+        assert torch.equal(got, want), cand
+    del a
+    torch.cuda.empty_cache()
