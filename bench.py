@@ -240,12 +240,19 @@ def run_gpu_arm(args, wl):
     from paper_1502_03504_b200 import runtime as R
 
     ws, rank, local = dist_env()
+    # one process per GPU; LOPE_BENCH_BACKEND=gloo lets a one-GPU box run the N>1 code
+    # path with all ranks sharing the device (a functional check, not a measurement)
+    backend = os.environ.get("LOPE_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     kir = stencils.by_name(wl["kernel"])
     kern = R.CompiledKernel(kir, wl["dtype"])
