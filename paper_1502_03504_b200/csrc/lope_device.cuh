@@ -292,6 +292,15 @@ __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
   const lope_u32 addr = lope_smem_u32(bar);
   lope_u32 done = 0, n = 0;
   do {
+#ifdef LOPE_WAIT_HINT_NS
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "n"(LOPE_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -299,6 +308,7 @@ __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
         : "=r"(done)
         : "r"(addr), "r"(parity)
         : "memory");
+#endif
     if (++n > LOPE_WAIT_LIMIT) __trap();
   } while (!done);
 }
