@@ -193,12 +193,12 @@ class PlanTuner:
     compute identical bits, so real steps double as measurements: each candidate
     runs ``STEPS`` consecutive steps (both ping-pong directions, as in steady
     state), timed with CUDA events on the launching stream, in ``PASSES``
-    round-robin passes; the fastest pass wins and becomes the plan
-    (``lope_plan_set``).  Timing a candidate on repeated launches in one direction
+    round-robin passes (forward, then reverse order); the lowest mean wins and
+    becomes the plan (``lope_plan_set``).  Timing a candidate on repeated launches in one direction
     ranks the plans differently (measured on B200), hence real alternating steps.
     """
 
-    STEPS = 2
+    STEPS = 6
     PASSES = 2
 
     def __init__(self, kernel: "CompiledKernel", layout, wrap_mask: int):
@@ -210,7 +210,10 @@ class PlanTuner:
         _lib.check(_lib.lib().lope_plan_candidates(kernel.handle, v, z, y, cap, ctypes.byref(n)),
                    "lope_plan_candidates")
         self.cands = [(int(v[i]), int(z[i]), int(y[i])) for i in range(min(n.value, cap))]
-        self.trials = [c for _ in range(self.PASSES) for c in range(len(self.cands))]
+        # passes alternate forward / reverse and scores are the mean over passes: the
+        # board's clocks drift during tuning (power ramp), a linear drift then cancels
+        order = list(range(len(self.cands)))
+        self.trials = [c for p in range(self.PASSES) for c in (order if p % 2 == 0 else order[::-1])]
         self.pos = 0
         self.sub = 0
         self.timed = []              # (candidate index, start event, end event)
@@ -246,10 +249,10 @@ class PlanTuner:
 
     def _finish(self) -> None:
         self.timed[-1][2].synchronize()
-        best = {}
+        acc = {}
         for c, a, b in self.timed:
-            ms = a.elapsed_time(b) / self.STEPS
-            best[c] = min(best.get(c, ms), ms)
+            acc.setdefault(c, []).append(a.elapsed_time(b) / self.STEPS)
+        best = {c: sum(v) / len(v) for c, v in acc.items()}
         ci = min(best, key=best.get)
         self._set(*self.cands[ci])
         desc = json.loads(self.kernel.describe())
