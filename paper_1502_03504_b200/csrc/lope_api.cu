@@ -72,6 +72,7 @@ struct Drv {
   decltype(&cuModuleGetGlobal) moduleGetGlobal = nullptr;
   decltype(&cuModuleUnload) moduleUnload = nullptr;
   decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
+  decltype(&cuFuncGetAttribute) funcGetAttribute = nullptr;
   decltype(&cuLaunchKernel) launchKernel = nullptr;
   decltype(&cuLaunchKernelEx) launchKernelEx = nullptr;   // optional (PDL launches)
   decltype(&cuMemGetAddressRange) memGetAddressRange = nullptr;   // optional (IPC export)
@@ -99,6 +100,7 @@ Drv& drv() {
          get("cuModuleGetGlobal", (void**)&d.moduleGetGlobal) &&
          get("cuModuleUnload", (void**)&d.moduleUnload) &&
          get("cuFuncSetAttribute", (void**)&d.funcSetAttribute) &&
+         get("cuFuncGetAttribute", (void**)&d.funcGetAttribute) &&
          get("cuLaunchKernel", (void**)&d.launchKernel) &&
          get("cuTensorMapEncodeTiled", (void**)&d.tensorMapEncodeTiled) &&
          get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occupancy) &&
@@ -298,6 +300,7 @@ struct DevMod {
   CUfunction generic = nullptr;
   CUfunction tiled = nullptr;
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
+  int tiled_local = 0;                  // local memory (spills) per thread of the tiled kernel
   CUfunction tblock = nullptr;          // temporal blocking (rank 2), variant 0 only
   int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0;
 };
@@ -577,6 +580,8 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     if (nb < 1) return fail(-4, "tiled kernel cannot be resident (smem %d B)", m.tiled_smem);
     m.tiled_blocks = nb;
+    int lb = 0;
+    if (d.funcGetAttribute(&lb, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, m.tiled) == CUDA_SUCCESS) m.tiled_local = lb;
   }
   if (d.moduleGetFunction(&m.tblock, m.mod, "lope_tblock") == CUDA_SUCCESS) {
     CUdeviceptr gp;
@@ -1210,6 +1215,16 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       // (y-banded walks, yband 4-16, measured no better on 1024^3 / 2048^3)
       for (int zc : {3, 4, 6, 8}) c.push_back({t, zc, 0});
     }
+    if (K->dtype == LOPE_F32) {
+      // 8 warps x 4 rows per lane: half the per-plane overhead per point
+      TileCfg t = base;
+      t.wy = 8;
+      t.ry = 4;
+      for (int zc : {32, 64}) c.push_back({t, zc, 0});
+      t.pw = 1;
+      t.ns = 12;
+      for (int zc : {3, 4, 6}) c.push_back({t, zc, 0});
+    }
   } else {
     c.push_back({base, 1, 0});
     for (int ns : {8, 12}) {
@@ -1372,6 +1387,9 @@ int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, in
     int vi = 0;
     if (int e = add_variant(k, cand.tile, &vi)) return e;
     if (!k->variants[vi].tiled_ok) continue;
+    DevMod* m = nullptr;
+    if (int e = get_mod(k, vi, &m)) return e;
+    if (m->tiled_local > 0) continue;   // spills go through L2 and cost halo reuse
     if (*n < cap && variants && zchunks && ybands) {
       variants[*n] = vi;
       zchunks[*n] = cand.zchunk;
