@@ -200,6 +200,7 @@ class PlanTuner:
 
     STEPS = 6
     PASSES = 2
+    WARM = 12       # untimed steps first: an idle GPU's clocks ramp up over the first ~ms
 
     def __init__(self, kernel: "CompiledKernel", layout, wrap_mask: int):
         self.kernel = kernel
@@ -216,6 +217,7 @@ class PlanTuner:
         self.trials = [c for p in range(self.PASSES) for c in (order if p % 2 == 0 else order[::-1])]
         self.pos = 0
         self.sub = 0
+        self.warm = self.WARM
         self.timed = []              # (candidate index, start event, end event)
         self._start = None
         self.report = {"candidates": [], "best": None}
@@ -223,19 +225,24 @@ class PlanTuner:
 
     @property
     def steps_needed(self) -> int:
-        return len(self.trials) * self.STEPS
+        return self.WARM + len(self.trials) * self.STEPS
 
     def _set(self, variant: int, zchunk: int, yband: int) -> None:
         _lib.check(_lib.lib().lope_plan_set(self.kernel.handle, ctypes.byref(self.layout), self.mask,
                                             variant, zchunk, yband), "lope_plan_set")
 
     def before(self, stream=None) -> None:
+        if self.warm > 0:
+            return
         if self.sub == 0:
             self._set(*self.cands[self.trials[self.pos]])
             self._start = _torch().cuda.Event(enable_timing=True)
             self._start.record(stream)
 
     def after(self, stream=None) -> None:
+        if self.warm > 0:
+            self.warm -= 1
+            return
         self.sub += 1
         if self.sub < self.STEPS:
             return
