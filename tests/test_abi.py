@@ -119,3 +119,24 @@ def test_machine_dropin_subclasses_the_reference_machine():
     assert issubclass(cls, lopec.runtime.Machine)
     for name in ("_launch", "_halo_exchange", "gather", "run"):
         assert getattr(cls, name) is not getattr(lopec.runtime.Machine, name), name
+
+
+def test_header_is_plain_c_and_the_c_driver_links(tmp_path):
+    """include/lope_b200.h compiles as C99 (no C++ or torch types in the boundary) and
+    tools/abi_bench.c -- a host that binds only the C ABI -- links against the library."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    cuda_inc = "/usr/local/cuda/include"
+    src = tmp_path / "use.c"
+    src.write_text('#include "lope_b200.h"\nint main(void) { return lope_abi_version() == 1 ? 0 : 1; }\n')
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-fsyntax-only", f"-I{REPO / 'include'}",
+                        f"-I{cuda_inc}", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = tmp_path / "abi_bench"
+    r = subprocess.run([gcc, "-O2", "-o", str(out), str(REPO / "tools" / "abi_bench.c"), f"-I{REPO / 'include'}",
+                        f"-I{cuda_inc}", f"-L{REPO / 'paper_1502_03504_b200'}", "-llope_b200",
+                        "-L/usr/local/cuda/lib64", "-lcudart"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
