@@ -302,7 +302,7 @@ struct DevMod {
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
   int tiled_local = 0;                  // local memory (spills) per thread of the tiled kernel
   CUfunction tblock = nullptr;          // temporal blocking (rank 2), variant 0 only
-  int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0;
+  int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0, tb_threads = 0;
 };
 
 // host mirrors of the device parameter structs (lope_device.cuh)
@@ -466,21 +466,24 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.pw << ">(&map, a, sc, g);\n"
       << "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   }
-  if (with_tblock && k.rank == 2 && k.arrays.size() == 1) {
-    // 128 x 28 fp32 tiles: 1024^2 splits into 296 = 2 x 148 CTAs (config 1, measured
-    // 2.27 us/step vs 2.47 at 32 rows); 8 steps per launch for one-cell footprints,
-    // 4 for wider ones (the recomputed halo grows with the footprint)
-    const int tx = K->dtype == LOPE_F32 ? 128 : 64;
+  if (with_tblock && k.rank == 2 && k.arrays.size() == 1 && k.fn[0][0] <= 4 && k.fp[0][0] <= 4) {
+    // 256 x 28 fp32 tiles: 1024^2 splits into 4 x 37 = 148 CTAs, one per SM (config 1);
+    // 8 steps per launch for one-cell footprints, 4 for wider ones (the recomputed
+    // halo grows with the footprint)
+    const int tx = K->dtype == LOPE_F32 ? 256 : 128;
     const int wmax = std::max(k.fn[0][0] + k.fp[0][0], k.fn[0][1] + k.fp[0][1]);
     int ty = 28, tt = wmax <= 2 ? 8 : 4;
     if (const char* e = std::getenv("LOPE_TBLOCK_TY")) ty = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("LOPE_TBLOCK_TT")) tt = std::max(1, std::atoi(e));
-    s << "typedef LopeTblockCfg<LopeBody, LT, " << tx << ", " << ty << ", " << tt << "> LopeTbCfg;\n";
-    s << "extern \"C\" __constant__ int lope_tblock_info[4] = {LopeTbCfg::SMEM_BYTES, " << tx << ", " << ty << ", "
-      << tt << "};\n";
-    s << "extern \"C\" __global__ void __launch_bounds__(1024) lope_tblock(const LopeArr<LT> a, "
-         "const LopeScal<LT> sc, const LopeGeom g) {\n"
-      << "  lope_tblock_impl<LopeBody, LT, " << tx << ", " << ty << ", " << tt << ">(a, sc, g);\n}\n";
+    const int vx = K->dtype == LOPE_F32 ? 4 : 2;
+    if ((tt * k.fn[0][0]) % vx == 0) {
+      s << "typedef LopeTblockCfg<LopeBody, LT, " << tx << ", " << ty << ", " << tt << "> LopeTbCfg;\n";
+      s << "extern \"C\" __constant__ int lope_tblock_info[5] = {LopeTbCfg::SMEM_BYTES, " << tx << ", " << ty
+        << ", " << tt << ", LopeTbCfg::THREADS};\n";
+      s << "extern \"C\" __global__ void __launch_bounds__(LopeTbCfg::THREADS) lope_tblock(const LopeArr<LT> a, "
+           "const LopeScal<LT> sc, const LopeGeom g) {\n"
+        << "  lope_tblock_impl<LopeBody, LT, " << tx << ", " << ty << ", " << tt << ">(a, sc, g);\n}\n";
+    }
   }
   return s.str();
 }
@@ -588,12 +591,13 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     size_t gsz;
     r = d.moduleGetGlobal(&gp, &gsz, m.mod, "lope_tblock_info");
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetGlobal(lope_tblock_info)");
-    int info[4];
+    int info[5];
     CUDA_TRY(cudaMemcpy(info, (const void*)gp, sizeof info, cudaMemcpyDeviceToHost));
     m.tb_smem = info[0];
     m.tb_tx = info[1];
     m.tb_ty = info[2];
     m.tb_tt = info[3];
+    m.tb_threads = info[4];
     r = d.funcSetAttribute(m.tblock, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tb_smem);
     if (r != CUDA_SUCCESS) m.tblock = nullptr;
   } else {
@@ -1272,7 +1276,9 @@ int lope_step_multi(const lope_kernel* kc, const lope_layout* layout, void* buf0
   DevMod* m = nullptr;
   if (int e = get_mod(k, 0, &m)) return e;
   const int full = (1 << ir.rank) - 1;
+  const int vxe = 16 / (int)layout->elem_bytes;
   const bool tb = m->tblock && ir.rank == 2 && !std::getenv("LOPE_NO_TBLOCK") &&
+                  layout->interior[0] % vxe == 0 && (m->tb_tt * ir.fn[0][0]) % vxe == 0 &&
                   layout->interior[0] >= m->tb_tx + m->tb_tt * (ir.fn[0][0] + ir.fp[0][0]) &&
                   layout->interior[1] >= m->tb_ty + m->tb_tt * (ir.fn[0][1] + ir.fp[0][1]);
   void* bufs[2] = {buf0, buf1};
@@ -1304,13 +1310,13 @@ int lope_step_multi(const lope_kernel* kc, const lope_layout* layout, void* buf0
         HArr<float> a{(const float*)bufs[live], (float*)bufs[1 - live], layout->stride[1], layout->stride[2], org};
         HScal<float> sc = make_scal<float>(ir, rscal, iscal);
         void* args[] = {&a, &sc, &g};
-        r = launch_ex(m->tblock, (unsigned)(ntx * nty), 1024, m->tb_smem, st, args);
+        r = launch_ex(m->tblock, (unsigned)(ntx * nty), (unsigned)m->tb_threads, m->tb_smem, st, args);
       } else {
         HArr<double> a{(const double*)bufs[live], (double*)bufs[1 - live], layout->stride[1], layout->stride[2],
                        org};
         HScal<double> sc = make_scal<double>(ir, rscal, iscal);
         void* args[] = {&a, &sc, &g};
-        r = launch_ex(m->tblock, (unsigned)(ntx * nty), 1024, m->tb_smem, st, args);
+        r = launch_ex(m->tblock, (unsigned)(ntx * nty), (unsigned)m->tb_threads, m->tb_smem, st, args);
       }
       if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tblock)");
       g_launches++;

@@ -745,115 +745,158 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
 // its periodic images.  Every point is evaluated with the same expression on the
 // same operands as the one-step kernel, so the bits are identical.
 
-template <class T, int W>
-struct LopeSmemTile2 {
-  const T* buf;
-  int bx, by;
-  template <int A, int DX, int DY, int DZ>
-  __device__ __forceinline__ T at() const { return buf[(by + DY) * W + bx + DX]; }
-};
-
 template <class Body, class T, int TX, int TY, int TT>
 struct LopeTblockCfg {
-  static constexpr int WI = TX + TT * (Body::FN0 + Body::FP0);
-  static constexpr int HI = TY + TT * (Body::FN1 + Body::FP1);
-  static constexpr int SMEM_BYTES = 2 * WI * HI * (int)sizeof(T);
+  static constexpr int VX = 16 / (int)sizeof(T);           // one 16-byte vector per lane
+  static constexpr int RY = 4;                              // rows per lane
+  static constexpr int WI = TX + TT * (Body::FN0 + Body::FP0);   // valid input columns
+  static constexpr int HI = TY + TT * (Body::FN1 + Body::FP1);   // valid input rows
+  static constexpr int PX = 4;                              // pad columns (>= footprint, vector aligned)
+  static constexpr int PY = (Body::FN1 > Body::FP1 ? Body::FN1 : Body::FP1);
+  static constexpr int NGX = (WI + VX - 1) / VX;            // vector groups per row
+  static constexpr int NGY = (HI + RY - 1) / RY;            // row groups
+  static constexpr int WB = NGX * VX + 2 * PX;              // buffer row pitch (elements)
+  static constexpr int HB = NGY * RY + 2 * PY;
+  static constexpr int THREADS = ((NGX * NGY + 31) / 32) * 32 > 1024 ? 1024 : ((NGX * NGY + 31) / 32) * 32;
+  static constexpr int SMEM_BYTES = 2 * WB * HB * (int)sizeof(T);
 };
 
+// Temporal blocking (rank 2, one array, every dim periodic): TT fused steps per
+// launch for fields that live in L2 (config 1), where a launch costs more than its
+// arithmetic.  Each CTA loads its tile plus TT footprints of halo (periodic indices
+// straight from the interior) into shared memory and advances it TT steps there --
+// the valid region shrinking by one footprint per step -- with the tiled kernel's
+// lane shape: a 16-byte vector of columns x 4 rows per lane, neighbours from a
+// register window filled by 16-byte loads.  Points outside the valid region are
+// computed from stale cells and never read by a valid point.  The last step stores
+// the tile and its periodic images.  Same expression on the same operands per point
+// as the one-step kernel, so the bits are identical.
 template <class Body, class T, int TX, int TY, int TT>
 __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const LopeScal<T>& sc, const LopeGeom& g) {
   typedef LopeTblockCfg<Body, T, TX, TY, TT> C;
+  typedef typename LopeVec<T>::V V;
   constexpr int FN0 = Body::FN0, FP0 = Body::FP0, FN1 = Body::FN1, FP1 = Body::FP1;
-  constexpr int WI = C::WI, HI = C::HI;
-  constexpr int NTX = TX, NTY = 1024 / TX;         // 1024 threads: a full tile row per row phase
+  constexpr int VX = C::VX, RY = C::RY, WI = C::WI, HI = C::HI, WB = C::WB, PX = C::PX, PY = C::PY;
+  constexpr int NR = RY + FN1 + FP1, NXW = VX + FN0 + FP0;
+  static_assert(FN0 <= PX && FP0 <= PX, "x footprint wider than the buffer pad");
+  static_assert((TT * FN0) % VX == 0, "the last step's tile must start on a vector");
   extern __shared__ __align__(16) unsigned char lope_smem[];
   T* b0 = reinterpret_cast<T*>(lope_smem);
-  T* b1 = b0 + WI * HI;
+  T* b1 = b0 + WB * C::HB;
   const int m0 = g.m[0], m1 = g.m[1];
   const int ntx = (m0 + TX - 1) / TX;
   const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-  const int x0 = tx * TX - TT * FN0, y0 = ty * TY - TT * FN1;   // interior coords of buffer (0,0)
-  const int cx = threadIdx.x % NTX, cy = threadIdx.x / NTX;
+  const int x0 = tx * TX - TT * FN0, y0 = ty * TY - TT * FN1;   // interior coords of valid cell (0,0)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // tile + TT halos, periodic indices straight from the interior (the host
-  // guarantees a tile plus TT halos fits in the interior: one wrap suffices)
+  // ---- load: tile + TT halos, periodic (the host guarantees one wrap suffices) ----
+  // 16-byte vectors: x0 and the interior width are multiples of VX (host), so a vector
+  // never straddles the periodic seam and wraps as a whole; all of a lane's loads are
+  // issued before the first shared store
   {
-    // all of this thread's loads in flight before the first shared store: columns
-    // cx, cx + NTX (wrapped once), rows cy, cy + NTY, ... (wrapped per row)
-    constexpr int NCOL = (WI + NTX - 1) / NTX, NROW = (HI + NTY - 1) / NTY;
-    int xw[NCOL];
+    constexpr int NV = C::NGX * HI;
+    constexpr int NLD = (NV + C::THREADS - 1) / C::THREADS;
+    V v[NLD];
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      int x = x0 + cx + c * NTX;
-      xw[c] = x + (x < 0 ? m0 : (x >= m0 ? -m0 : 0));
-    }
-    T v[NROW][NCOL];
-#pragma unroll
-    for (int r = 0; r < NROW; ++r) {
-      const int by = cy + r * NTY;
-      int y = y0 + by;
-      y += y < 0 ? m1 : (y >= m1 ? -m1 : 0);
-      const T* row = a.in + a.org + (lope_i64)y * a.s1;
-#pragma unroll
-      for (int c = 0; c < NCOL; ++c)
-        if (by < HI && cx + c * NTX < WI) v[r][c] = __ldg(row + xw[c]);
-    }
-#pragma unroll
-    for (int r = 0; r < NROW; ++r)
-#pragma unroll
-      for (int c = 0; c < NCOL; ++c) {
-        const int by = cy + r * NTY, bx = cx + c * NTX;
-        if (by < HI && bx < WI) b0[by * WI + bx] = v[r][c];
+    for (int k = 0; k < NLD; ++k) {
+      const int p = threadIdx.x + k * C::THREADS;
+      if (p < NV) {
+        const int gx = p % C::NGX, by = p / C::NGX;
+        int x = x0 + gx * VX, y = y0 + by;
+        x += x < 0 ? m0 : (x >= m0 ? -m0 : 0);
+        y += y < 0 ? m1 : (y >= m1 ? -m1 : 0);
+        v[k] = __ldg(reinterpret_cast<const V*>(a.in + a.org + x + (lope_i64)y * a.s1));
       }
+    }
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int p = threadIdx.x + k * C::THREADS;
+      if (p < NV) {
+        const int gx = p % C::NGX, by = p / C::NGX;
+        *reinterpret_cast<V*>(b0 + (by + PY) * WB + gx * VX + PX) = v[k];
+      }
+    }
   }
   __syncthreads();
-#pragma unroll
-  for (int s = 1; s < TT; ++s) {
+  const bool wxm = g.wrap & 1, wym = (g.wrap >> 1) & 1;
+#pragma unroll 1
+  for (int s = 1; s <= TT; ++s) {
     const T* src = (s & 1) ? b0 : b1;
     T* dst = (s & 1) ? b1 : b0;
-    for (int by = s * FN1 + cy; by < HI - s * FP1; by += NTY)
-      for (int bx = s * FN0 + cx; bx < WI - s * FP0; bx += NTX) {
-        LopeSmemTile2<T, WI> rd;
-        rd.buf = src;
-        rd.bx = bx;
-        rd.by = by;
-        T res[1];
-        bool slow = false;
-        Body::template eval<T, false>(rd, sc.v, res, slow);
-        dst[by * WI + bx] = res[0];
+    // lanes cover the vector groups / row groups that intersect this step's valid region
+    const int gx0 = (s * FN0) / VX, gx1 = (WI - s * FP0 + VX - 1) / VX;
+    const int gy0 = (s * FN1) / RY, gy1 = (HI - s * FP1 + RY - 1) / RY;
+    const int ngx = gx1 - gx0, ntask = ngx * (gy1 - gy0);
+    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+      const int bx = (gx0 + t % ngx) * VX, by = (gy0 + t / ngx) * RY;
+      const T* base = src + (by + PY) * WB + bx + PX;
+      T win[1][NR][NXW];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const T* rp = base + (q - FN1) * WB;
+        const V vv = *reinterpret_cast<const V*>(rp);
+        const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+        for (int e = 0; e < VX; ++e) win[0][q][FN0 + e] = ve[e];
+#pragma unroll
+        for (int e = 1; e <= FN0; ++e) win[0][q][FN0 - e] = rp[-e];
+#pragma unroll
+        for (int e = 0; e < FP0; ++e) win[0][q][FN0 + VX + e] = rp[VX + e];
       }
-    __syncthreads();
-  }
-  // last step: the tile itself, stored with its periodic images
-  const T* src = (TT & 1) ? b0 : b1;
-  const bool wx = g.wrap & 1, wy = (g.wrap >> 1) & 1;
-  for (int by = TT * FN1 + cy; by < TT * FN1 + TY; by += NTY) {
-    const int y = y0 + by;
-    if (y >= m1) break;
-    const bool yh = wy && y < g.hi[1], yl = wy && y >= m1 - g.lo[1];
-    const lope_i64 yimg = (yh ? (lope_i64)m1 : -(lope_i64)m1) * a.s1;
-    T* orow = a.out + a.org + (lope_i64)y * a.s1;
-    for (int bx = TT * FN0 + cx; bx < TT * FN0 + TX; bx += NTX) {
-      const int x = x0 + bx;
-      if (x >= m0) break;
-      LopeSmemTile2<T, WI> rd;
-      rd.buf = src;
-      rd.bx = bx;
-      rd.by = by;
-      T res[1];
-      bool slow = false;
-      Body::template eval<T, false>(rd, sc.v, res, slow);
-      orow[x] = res[0];
-      const bool xh = wx && x < g.hi[0], xl = wx && x >= m0 - g.lo[0];
-      if (xh | xl | yh | yl) {
-        const int ximg = xh ? m0 : -m0;
-        if (xh | xl) orow[x + ximg] = res[0];
-        if (yh | yl) {
-          orow[x + yimg] = res[0];
-          if (xh | xl) orow[x + ximg + yimg] = res[0];
+      T vals[RY][VX];
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int v = 0; v < VX; ++v) {
+          LopeWinReader<T, NR, NXW, 0, FN0, FN1, RY, VX, false> rd;
+          rd.win = &win[0][0][0];
+          rd.hist = nullptr;
+          rd.r = r;
+          rd.v = v;
+          T res[1];
+          bool slow = false;
+          Body::template eval<T, false>(rd, sc.v, res, slow);
+          vals[r][v] = res[0];
+        }
+      if (s < TT) {
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          V o;
+          T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+          *reinterpret_cast<V*>(dst + (by + r + PY) * WB + bx + PX) = o;
+        }
+      } else {
+        // the tile itself: interior stores plus the periodic images of boundary cells
+        const int x = x0 + bx;
+        if (bx < TT * FN0 || bx >= TT * FN0 + TX || x >= m0) continue;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const int yb = by + r, y = y0 + yb;
+          if (yb < TT * FN1 || yb >= TT * FN1 + TY || y >= m1) continue;
+          T* orow = a.out + a.org + (lope_i64)y * a.s1;
+          const bool yh = wym && y < g.hi[1], yl = wym && y >= m1 - g.lo[1];
+          const lope_i64 yimg = (yh ? (lope_i64)m1 : -(lope_i64)m1) * a.s1;
+#pragma unroll
+          for (int e = 0; e < VX; ++e) {
+            const int xe = x + e;
+            if (xe >= m0) break;
+            const T v = vals[r][e];
+            orow[xe] = v;
+            const bool xh = wxm && xe < g.hi[0], xl = wxm && xe >= m0 - g.lo[0];
+            if (xh | xl | yh | yl) {
+              const int ximg = xh ? m0 : -m0;
+              if (xh | xl) orow[xe + ximg] = v;
+              if (yh | yl) {
+                orow[xe + yimg] = v;
+                if (xh | xl) orow[xe + ximg + yimg] = v;
+              }
+            }
+          }
         }
       }
     }
+    __syncthreads();
   }
 }

@@ -306,10 +306,11 @@ def test_plan_tuning_is_bitwise_transparent(name, shape, dt):
 @pytest.mark.parametrize("name,shape,dt,n", [("heat2d", (1024, 1024), "float32", 17),
                                              ("heat2d", (300, 170), "float64", 17),
                                              ("box5x5", (256, 192), "float64", 8),
-                                             ("drift2", (200, 160), "float32", 16),
-                                             ("ninept2d", (144, 44), "float32", 17),
-                                             ("box5x5", (160, 64), "float32", 12),
-                                             ("heat2d", (100, 60), "float32", 6)])
+                                             ("drift2", (288, 160), "float32", 16),
+                                             ("ninept2d", (272, 44), "float32", 17),
+                                             ("box5x5", (288, 64), "float32", 12),
+                                             ("heat2d", (100, 60), "float32", 6),
+                                             ("heat2d", (1000, 333), "float32", 16)])
 def test_temporal_blocking_is_bitwise_identical(monkeypatch, name, shape, dt, n):
     """multi_step (4 steps per launch in shared memory for rank 2) leaves the same
     padded block -- interior and periodic halo images -- as n single fused steps."""
