@@ -771,17 +771,21 @@ class PeerSlabStepper:
         prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
         self._opened = []
         self.peers = {}
-        for who in sorted({prev, nxt}):
-            ptrs = []
-            for (h, off) in allh[who]:
-                if who == self.rank:
-                    ptrs = [b.data_ptr() for b in blk._bufs]
-                    break
-                p = ctypes.c_void_p()
-                _lib.check(_lib.lib().lope_ipc_open(h, off, ctypes.byref(p)), "lope_ipc_open")
-                self._opened.append(p.value)
-                ptrs.append(p.value)
-            self.peers[who] = ptrs
+        try:
+            for who in sorted({prev, nxt}):
+                ptrs = []
+                for (h, off) in allh[who]:
+                    if who == self.rank:
+                        ptrs = [b.data_ptr() for b in blk._bufs]
+                        break
+                    p = ctypes.c_void_p()
+                    _lib.check(_lib.lib().lope_ipc_open(h, off, ctypes.byref(p)), "lope_ipc_open")
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                self.peers[who] = ptrs
+        except Exception:
+            self.close()          # unmap whatever was mapped before the failure
+            raise
         self.prev, self.next = prev, nxt
         d = arr.dim
         L = blk.layout
