@@ -206,7 +206,7 @@ def run_reference_arm(args, wl):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
+    import numpy as np
     steps, warm = args.steps, args.warmup
     # each step: a bounded CPU sample; scale to a few minutes in total
     per = max(0.5, min(5.0, 120.0 / max(1, steps + warm)))
@@ -215,7 +215,10 @@ def run_reference_arm(args, wl):
     line = {
         "metric": "stencil Gpoints/s & HBM GB/s (% of 8 TB/s roofline) at 1/2/4/8 B200 vs CPU ref",
         "impl": "reference", "value": res["value"], "unit": "Gpoints/s", "n_gpus": ws,
-        "steps": steps, "warmup": warm, "ms_per_step": None, "higher_is_better": True,
+        "steps": steps, "warmup": warm,
+        # the sample's rate extrapolated to one step over the whole workload
+        "ms_per_step": round(float(np.prod(wl["shape"])) / res["value"] / 1e6, 3) if res.get("value") else None,
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "float32" else "f64",
         "data": "synthetic (splitmix64 U(-1,1) field)",
         "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
