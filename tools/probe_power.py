@@ -6,8 +6,10 @@ if os.environ.get("TUNE") != "1":
 import torch, numpy as np, pynvml
 from paper_1502_03504_b200 import runtime as R, stencils
 shape = tuple(int(x) for x in os.environ.get("SHAPE", "1024,1024,1024").split(","))
-k = R.CompiledKernel(stencils.by_name(os.environ.get("KERNEL", "lap3d7")), os.environ.get("DT", "float32"))
-a = R.HaloArray(shape, [1] * len(shape), [1] * len(shape), os.environ.get("DT", "float32"))
+kir = stencils.by_name(os.environ.get("KERNEL", "lap3d7"))
+k = R.CompiledKernel(kir, os.environ.get("DT", "float32"))
+fp = kir.footprints[kir.array_params[0]].dims
+a = R.HaloArray(shape, [n for n, _ in fp], [p for _, p in fp], os.environ.get("DT", "float32"))
 a.fill_hash(1); R.halo_transfer(a)
 n = int(os.environ.get("N", "800"))
 pynvml.nvmlInit(); h = pynvml.nvmlDeviceGetHandleByIndex(0)
