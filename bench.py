@@ -54,6 +54,7 @@ WORKLOADS = {
                desc="3D 7-point 2048^3 fp32 per GPU, halo 1 (config 5, weak scaling)"),
 }
 E2E_ITERS = 100
+WARM_SECONDS = 0.5
 SEED = 20260823
 
 
@@ -301,13 +302,33 @@ def run_gpu_arm(args, wl):
     # plan selection (runtime.PlanTuner): real steps under each candidate plan, part
     # of setup like compilation; the timed steps run the chosen plan
     tune_steps = 0
+    t_tune = time.perf_counter()
     if ws > 1:
         tune_steps = stepper.tune()
     else:
-        while kern.tuner(arr, (1 << arr.rank) - 1) is not None:
+        while kern.tuning(arr, (1 << arr.rank) - 1):
             do_step()
             tune_steps += 1
+    torch.cuda.synchronize()
+    tune_secs = time.perf_counter() - t_tune
+    t_w = time.perf_counter()
     for _ in range(args.warmup):
+        do_step()
+    torch.cuda.synchronize()
+    warm_secs = time.perf_counter() - t_w
+    # the board needs a few hundred ms of load before its clocks settle (B200: the first
+    # ~100-200 steps of config 3 run ~25% slower): extra untimed steps until
+    # the warm-up (tuning included) has lasted WARM_SECONDS -- a step count every rank
+    # agrees on, since the multi-GPU steps synchronise
+    step_est = warm_secs / max(1, args.warmup)
+    extra = int(math.ceil(max(0.0, WARM_SECONDS - tune_secs - warm_secs) / max(step_est, 1e-6)))
+    extra = min(extra, 10000)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([extra], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra = int(t.item())
+    for _ in range(extra):
         do_step()
     torch.cuda.synchronize()
     graph = None
@@ -399,7 +420,9 @@ def run_gpu_arm(args, wl):
                        "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
                              else "L2-resident working set (config 1); HBM fraction informational",
                        "hbm_gbs_alg": round(alg_bytes * ws / (ms_per_step / 1e3) / 1e9 / ws, 1)},
-            "plan": {"chosen": json.loads(kern.describe()).get("plans"), "tuning_steps": tune_steps},
+            "plan": {"chosen": json.loads(kern.describe()).get("plans"), "tuning_steps": tune_steps,
+                     "extra_warmup_steps": extra,
+                     "watchdog_fallback": [t.report.get("fallback") for t in kern._tuners.values()]},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -173,6 +173,10 @@ int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, in
                          int32_t* n);
 int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk,
                   int32_t yband);
+/* The same with the variant named by its tile shape {bxw, wy, ry, ns, producer_warp,
+ * ctas_per_sm} (compiled if needed); *variant (may be NULL) receives its index. */
+int lope_plan_set_tile(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, const int32_t* tile,
+                       int32_t zchunk, int32_t yband, int32_t* variant);
 
 /* Box <-> contiguous device buffer (column-major within the box, dim 1 fastest):
  * `extent` cells at padded coordinates `lo`.  Faces of a decomposed dimension other

@@ -1410,6 +1410,25 @@ int lope_plan_candidates(lope_kernel* k, int32_t* variants, int32_t* zchunks, in
   return 0;
 }
 
+int lope_plan_set_tile(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, const int32_t* tile,
+                       int32_t zchunk, int32_t yband, int32_t* variant) {
+  if (!k || !layout || !tile) return fail(108, "null argument");
+  if (int e = check_layout(layout)) return e;
+  TileCfg c;
+  c.bxw = tile[0];
+  c.wy = tile[1];
+  c.ry = tile[2];
+  c.ns = tile[3];
+  c.pw = tile[4] ? 1 : 0;
+  c.mb = tile[5] == 2 ? 2 : 1;
+  if (c.bxw < 1 || c.wy < 1 || c.ry < 1 || c.ns < 2) return fail(108, "bad tile shape");
+  int vi = 0;
+  if (int e = add_variant(k, c, &vi)) return e;
+  if (!k->variants[vi].tiled_ok) return fail(108, "tile variant does not fit shared memory");
+  if (variant) *variant = vi;
+  return lope_plan_set(k, layout, wrap_mask, vi, zchunk, yband);
+}
+
 int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk,
                   int32_t yband) {
   if (!k || !layout) return fail(108, "null argument");

@@ -254,7 +254,7 @@ class SlabStepper:
     def tune(self) -> int:
         """Run real steps until the plan for this slab is chosen; returns the count."""
         n = 0
-        while self.kernel.tuner(self.arr.block, self.arr.local_mask) is not None:
+        while self.kernel.tuning(self.arr.block, self.arr.local_mask):
             self.step()
             n += 1
         return n
@@ -832,7 +832,7 @@ class PeerSlabStepper:
     def tune(self) -> int:
         """Run real steps until the plan for this block is chosen; returns the count."""
         n = 0
-        while self.kernel.tuner(self.arr.block, self.full) is not None:
+        while self.kernel.tuning(self.arr.block, self.full):
             self.step()
             n += 1
         return n

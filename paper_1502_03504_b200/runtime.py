@@ -196,11 +196,21 @@ class PlanTuner:
     round-robin passes (forward, then reverse order); the lowest mean wins and
     becomes the plan (``lope_plan_set``).  Timing a candidate on repeated launches in one direction
     ranks the plans differently (measured on B200), hence real alternating steps.
+
+    Watchdog: the short-z-chunk plans have a slow mode (same plan, same buffers, 25-30%
+    slower for hundreds of steps, entered and left unpredictably -- see DESIGN §9).
+    When the winner is such a plan, the tuner keeps timing every step (events queried
+    without blocking) and falls back to the best long-chunk plan once the median of
+    the last ``WATCH`` steps is ``SLOW`` times the winner's fastest observed step time
+    (its fast mode; the slow mode is >= 1.25x, the power cap alone costs <= 1.1x).
     """
 
     STEPS = 6
     PASSES = 2
     WARM = 12       # untimed steps first: an idle GPU's clocks ramp up over the first ~ms
+    WATCH = 12      # steps in the watchdog's window
+    SLOW = 1.2      # watchdog threshold relative to the winner's tuned time
+    SAFE_ZCHUNK = 16  # plans with at least this many planes per unit have no slow mode
 
     def __init__(self, kernel: "CompiledKernel", layout, wrap_mask: int):
         self.kernel = kernel
@@ -222,6 +232,10 @@ class PlanTuner:
         self._start = None
         self.report = {"candidates": [], "best": None}
         self.done = len(self.cands) <= 1
+        self.monitoring = False
+        self._watch = []             # (start, end) events of recent steps, oldest first
+        self._durations = []
+        self._safe = None            # (candidate, tuned ms) of the best long-chunk plan
 
     @property
     def steps_needed(self) -> int:
@@ -231,7 +245,16 @@ class PlanTuner:
         _lib.check(_lib.lib().lope_plan_set(self.kernel.handle, ctypes.byref(self.layout), self.mask,
                                             variant, zchunk, yband), "lope_plan_set")
 
+    @property
+    def active(self) -> bool:
+        return not self.done or self.monitoring
+
     def before(self, stream=None) -> None:
+        if self.done:
+            if self.monitoring:
+                self._start = _torch().cuda.Event(enable_timing=True)
+                self._start.record(stream)
+            return
         if self.warm > 0:
             return
         if self.sub == 0:
@@ -240,6 +263,10 @@ class PlanTuner:
             self._start.record(stream)
 
     def after(self, stream=None) -> None:
+        if self.done:
+            if self.monitoring:
+                self._watch_step(stream)
+            return
         if self.warm > 0:
             self.warm -= 1
             return
@@ -262,13 +289,43 @@ class PlanTuner:
         best = {c: sum(v) / len(v) for c, v in acc.items()}
         ci = min(best, key=best.get)
         self._set(*self.cands[ci])
+        safe = [c for c in best if self.cands[c][1] >= self.SAFE_ZCHUNK]
+        if self.cands[ci][1] < self.SAFE_ZCHUNK and safe:
+            cs = min(safe, key=best.get)
+            self._safe = (cs, min(acc[ci]))     # the winner's fastest trial: its fast mode
+            self.monitoring = True
         desc = json.loads(self.kernel.describe())
         self.report = {"candidates": [list(self.cands[c]) + [round(best[c], 5)] for c in sorted(best)],
                        "best": {"variant": self.cands[ci][0], "zchunk": self.cands[ci][1],
                                 "yband": self.cands[ci][2], "ms_per_step": round(best[ci], 5)},
-                       "plans": desc.get("plans")}
+                       "plans": desc.get("plans"), "fallback": None}
         self.timed = []
         self.done = True
+
+    def _watch_step(self, stream) -> None:
+        end = _torch().cuda.Event(enable_timing=True)
+        end.record(stream)
+        self._watch.append((self._start, end))
+        while self._watch and self._watch[0][1].query():      # completed: no host stall
+            a, b = self._watch.pop(0)
+            self._durations.append(a.elapsed_time(b))
+        self._check_window()
+
+    def _check_window(self) -> None:
+        """Fall back to the long-chunk plan if the recent steps are in the slow mode."""
+        self._durations = self._durations[-self.WATCH:]
+        if self._durations:
+            cs, fast_ms = self._safe
+            self._safe = (cs, min(fast_ms, min(self._durations)))
+        if len(self._durations) == self.WATCH:
+            med = sorted(self._durations)[self.WATCH // 2]
+            cs, tuned_ms = self._safe
+            if med > self.SLOW * tuned_ms:
+                self._set(*self.cands[cs])
+                self.monitoring = False
+                self._watch = []
+                self.report["fallback"] = {"to": list(self.cands[cs]), "median_ms": round(med, 5),
+                                           "tuned_ms": round(tuned_ms, 5)}
 
 
 class CompiledKernel:
@@ -305,16 +362,25 @@ class CompiledKernel:
     def tuner(self, arr: "HaloArray", wrap_mask: int) -> Optional["PlanTuner"]:
         """The online plan tuner for ``arr``'s geometry while it is still measuring
         (None once a plan is chosen, for small blocks, with ``LOPE_AUTOTUNE=0`` and
-        during CUDA-graph capture)."""
+        during CUDA-graph capture).  There is deliberately no offline plan table: the
+        short-z-chunk plans' speed depends on where the buffers sit in HBM (the plan
+        that ran 1.49 ms sustained on one allocation ran 1.88 ms on another), so the
+        plan is measured on the live buffers."""
         key = _tune_key(arr, wrap_mask)
         t = self._tuners.get(key)
         if t is None:
             if not _autotune_enabled() or arr.layout.count < _AUTOTUNE_MIN_CELLS:
                 return None
             t = self._tuners[key] = PlanTuner(self, arr.layout, wrap_mask)
-        if t.done or _torch().cuda.is_current_stream_capturing():
+        if not t.active or _torch().cuda.is_current_stream_capturing():
             return None
         return t
+
+    def tuning(self, arr: "HaloArray", wrap_mask: int) -> bool:
+        """True while the plan for ``arr``'s geometry is still being measured (the
+        watchdog that may follow does not count)."""
+        t = self.tuner(arr, wrap_mask)
+        return t is not None and not t.done
 
     def tune(self, arr: "HaloArray", scalars=None, wrap_mask: Optional[int] = None, stream=None) -> dict:
         """Choose the plan for ``arr``'s geometry now by running real fused steps under

@@ -140,3 +140,24 @@ def test_header_is_plain_c_and_the_c_driver_links(tmp_path):
                         f"-I{cuda_inc}", f"-L{REPO / 'paper_1502_03504_b200'}", "-llope_b200",
                         "-L/usr/local/cuda/lib64", "-lcudart"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_plan_watchdog_falls_back_only_on_the_slow_mode():
+    """PlanTuner's watchdog (CPU logic): a window of steps >= SLOW x the fast-mode time
+    switches to the long-chunk plan; power-cap-sized slowdowns do not."""
+    from paper_1502_03504_b200.runtime import PlanTuner
+    t = PlanTuner.__new__(PlanTuner)
+    t.cands = [(0, 64, 0), (2, 6, 0)]
+    t.report = {"fallback": None}
+    t._watch = []
+    calls = []
+    t._set = lambda *c: calls.append(c)
+    # fast mode 1.40 ms, power cap pushes steps to 1.52 ms: keep the plan
+    t._safe, t.monitoring, t._durations = (0, 1.40), True, [1.52] * PlanTuner.WATCH
+    t._check_window()
+    assert t.monitoring and not calls and t.report["fallback"] is None
+    # slow mode (1.95 ms): fall back to the long-chunk candidate 0
+    t._durations = [1.95] * PlanTuner.WATCH
+    t._check_window()
+    assert not t.monitoring and calls == [(0, 64, 0)]
+    assert t.report["fallback"]["to"] == [0, 64, 0]
