@@ -293,6 +293,7 @@ struct TileCfg {
   int bxw = 4, wy = 2, ry = 8, ns = 8;
   int mb = 2;     // CTAs per SM the launch bounds target
   int pw = 0;     // 1: dedicated TMA producer warp
+  int sh = 0;     // 1: x-halo columns through warp shuffles (fp32, one-column halos)
 };
 
 struct DevMod {
@@ -435,6 +436,7 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
   }
   if (const char* e = std::getenv("LOPE_MB")) c.mb = std::atoi(e) == 2 ? 2 : 1;
   if (const char* e = std::getenv("LOPE_PW")) c.pw = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("LOPE_SHFL")) c.sh = std::atoi(e) ? 1 : 0;
   if (c.ns < hold + 1) c.ns = hold + 1;
   // shrink the ring until mb CTAs fit on an SM (227 KB)
   while (c.ns > hold + 1 && c.mb * tiled_smem_bytes(k, dtype, c) > 225 * 1024) --c.ns;
@@ -463,7 +465,7 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.mb << ") lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
-      << ", " << c.pw << ">(&map, a, sc, g);\n"
+      << ", " << c.pw << ", " << c.sh << ">(&map, a, sc, g);\n"
       << "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1 && k.fn[0][0] <= 4 && k.fp[0][0] <= 4) {
@@ -612,7 +614,8 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
 int add_variant(lope_kernel* K, const TileCfg& cfg, int* vi = nullptr) {
   for (size_t i = 0; i < K->variants.size(); ++i) {
     const TileCfg& c = K->variants[i].tile;
-    if (c.bxw == cfg.bxw && c.wy == cfg.wy && c.ry == cfg.ry && c.ns == cfg.ns && c.mb == cfg.mb && c.pw == cfg.pw) {
+    if (c.bxw == cfg.bxw && c.wy == cfg.wy && c.ry == cfg.ry && c.ns == cfg.ns && c.mb == cfg.mb && c.pw == cfg.pw &&
+        c.sh == cfg.sh) {
       if (vi) *vi = (int)i;
       return 0;
     }
@@ -1044,7 +1047,7 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
   for (const auto& kv : k->plans) {
     const TileCfg& c = k->variants[kv.second.variant].tile;
     o << (first ? "" : ",") << "\"" << kv.first << "\":{\"tile\":[" << c.bxw << "," << c.wy << "," << c.ry << ","
-      << c.ns << "],\"producer_warp\":" << c.pw << ",\"zchunk\":" << kv.second.zchunk << ",\"yband\":" << kv.second.yband
+      << c.ns << "],\"producer_warp\":" << c.pw << ",\"shfl\":" << c.sh << ",\"zchunk\":" << kv.second.zchunk << ",\"yband\":" << kv.second.yband
       << "}";
     first = false;
   }
@@ -1216,6 +1219,7 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       TileCfg t = base;
       t.pw = 1;
       t.ns = ns;
+      t.sh = 1;
       // (y-banded walks, yband 4-16, measured no better on 1024^3 / 2048^3)
       for (int zc : {3, 4, 6, 8}) c.push_back({t, zc, 0});
     }
@@ -1227,6 +1231,7 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       for (int zc : {32, 64}) c.push_back({t, zc, 0});
       t.pw = 1;
       t.ns = 12;
+      t.sh = 1;
       for (int zc : {3, 4, 6}) c.push_back({t, zc, 0});
     }
   } else {

@@ -437,7 +437,7 @@ struct LopeUnitWalk {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0, int SH = 0>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
   typedef LopeTiledCfg<Body, T, WX, WY, RY, NS, PW> C;
@@ -610,10 +610,33 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           const T* ve = reinterpret_cast<const T*>(&vv);
 #pragma unroll
           for (int e = 0; e < VX; ++e) win[k][q][Body::FN0 + e] = ve[e];
+          // x halo: with SH the neighbouring lanes' vectors supply those columns (warp
+          // shuffles, no bank conflicts; only the warp's edge lanes read shared memory) --
+          // a plan parameter: it moves the timing of the short-z-chunk plans out of their
+          // slow mode (1.86 -> 1.41 ms) but costs the in-band plan 12% (1.51 -> 1.69 ms)
 #pragma unroll
-          for (int e = 1; e <= Body::FN0; ++e) win[k][q][Body::FN0 - e] = rp[-e];
+          for (int e = 1; e <= Body::FN0; ++e) {
+            T hv;
+            // one-column halos in fp32 only: wider ones (5x5 box) spill with the shuffles
+            if (SH && sizeof(T) == 4 && Body::FN0 <= 1 && Body::FP0 <= 1) {
+              hv = __shfl_up_sync(0xffffffffu, ve[VX - e], 1);
+              if (lane == 0) hv = rp[-e];
+            } else {
+              hv = rp[-e];
+            }
+            win[k][q][Body::FN0 - e] = hv;
+          }
 #pragma unroll
-          for (int e = 0; e < Body::FP0; ++e) win[k][q][Body::FN0 + VX + e] = rp[VX + e];
+          for (int e = 0; e < Body::FP0; ++e) {
+            T hv;
+            if (SH && sizeof(T) == 4 && Body::FN0 <= 1 && Body::FP0 <= 1) {
+              hv = __shfl_down_sync(0xffffffffu, ve[e], 1);
+              if (lane == 31) hv = rp[VX + e];
+            } else {
+              hv = rp[VX + e];
+            }
+            win[k][q][Body::FN0 + VX + e] = hv;
+          }
         }
         const int r = q - Body::FN1 - Body::FP1;
         if (r >= 0) {
@@ -833,9 +856,16 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
     const int gx0 = (s * FN0) / VX, gx1 = (WI - s * FP0 + VX - 1) / VX;
     const int gy0 = (s * FN1) / RY, gy1 = (HI - s * FP1 + RY - 1) / RY;
     const int ngx = gx1 - gx0, ntask = ngx * (gy1 - gy0);
+    const int lane = threadIdx.x & 31;
     for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
-      const int bx = (gx0 + t % ngx) * VX, by = (gy0 + t / ngx) * RY;
+      const int gxi = t % ngx;
+      const int bx = (gx0 + gxi) * VX, by = (gy0 + t / ngx) * RY;
       const T* base = src + (by + PY) * WB + bx + PX;
+      // active lanes are a prefix of the warp (contiguous tasks); the x halo comes from
+      // the neighbouring lane unless that lane is another row, another warp or idle
+      const unsigned am = __activemask();
+      const bool own_l = lane == 0 || gxi == 0;
+      const bool own_r = lane == 31 || gxi == ngx - 1 || t + 1 >= ntask;
       T win[1][NR][NXW];
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
@@ -845,9 +875,27 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
 #pragma unroll
         for (int e = 0; e < VX; ++e) win[0][q][FN0 + e] = ve[e];
 #pragma unroll
-        for (int e = 1; e <= FN0; ++e) win[0][q][FN0 - e] = rp[-e];
+        for (int e = 1; e <= FN0; ++e) {
+          T hv;
+          if (FN0 <= VX) {
+            hv = __shfl_up_sync(am, ve[VX - e], 1);
+            if (own_l) hv = rp[-e];
+          } else {
+            hv = rp[-e];
+          }
+          win[0][q][FN0 - e] = hv;
+        }
 #pragma unroll
-        for (int e = 0; e < FP0; ++e) win[0][q][FN0 + VX + e] = rp[VX + e];
+        for (int e = 0; e < FP0; ++e) {
+          T hv;
+          if (FP0 <= VX) {
+            hv = __shfl_down_sync(am, ve[e], 1);
+            if (own_r) hv = rp[VX + e];
+          } else {
+            hv = rp[VX + e];
+          }
+          win[0][q][FN0 + VX + e] = hv;
+        }
       }
       T vals[RY][VX];
 #pragma unroll
