@@ -318,6 +318,18 @@ __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
     if (++n > LOPE_WAIT_LIMIT) __trap();
   } while (!done);
 }
+// Non-blocking probe of a barrier phase (mbarrier.test_wait).
+__device__ __forceinline__ bool lope_mbar_test(lope_u64* bar, lope_u32 parity) {
+  lope_u32 done = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(done)
+      : "r"(lope_smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
 __device__ __forceinline__ void lope_tma_load_3d(void* dst, const LopeTmap* map, lope_u64* bar, int c0,
                                                  int c1, int c2) {
   asm volatile(
@@ -437,7 +449,7 @@ struct LopeUnitWalk {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0, int SH = 0>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0, int SH = 0, int NB = 0>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
   typedef LopeTiledCfg<Body, T, WX, WY, RY, NS, PW> C;
@@ -499,10 +511,17 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
       p_z = oz + z0;
     }
   }
-  auto produce = [&](lope_u32 limit) {
+  // Loads below `needed` are waited for (the issuing warp reads them next); loads up to
+  // `limit` are prefetch and only issued while their slot is already free, so the
+  // in-band producer never stalls warp 0 on a slower warp just to run further ahead.
+  auto produce = [&](lope_u32 needed, lope_u32 limit) {
     while (p_L < limit && p_u < nunits) {
       const lope_u32 slot = p_L % NS;
-      if (p_L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((p_L / NS) - 1) & 1);
+      if (p_L >= (lope_u32)NS) {
+        const lope_u32 par = ((p_L / NS) - 1) & 1;
+        if (p_L < needed) lope_mbar_wait(&empty[slot], par);
+        else if (!lope_mbar_test(&empty[slot], par)) break;
+      }
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
       if (g.p1 > 0)
         lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
@@ -526,7 +545,7 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
 
   if (PW && warp == C::NCW) {
     // dedicated producer warp: issue everything, slot by slot
-    if (lane == 0) produce(0xffffffffu);
+    if (lane == 0) produce(0xffffffffu, 0xffffffffu);
     return;
   }
 
@@ -567,7 +586,9 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
     for (int pz = 0; pz < nz; ++pz, orow += s2) {
       // ---- top up the TMA ring (warp 0 lane 0) ----
       if (!PW && warp == 0) {
-        if (lane == 0) produce((ZHIST ? (pz == 0 ? lbase : lbase + pz + FZN) : lbase + pz) + NS);
+        if (lane == 0)
+          produce(NB ? lbase + pz + NZW : 0xffffffffu,
+                  (ZHIST ? (pz == 0 ? lbase : lbase + pz + FZN) : lbase + pz) + NS);
         __syncwarp();
       }
       // ---- wait for the planes this iteration reads ----
