@@ -759,18 +759,27 @@ class PeerSlabStepper:
         self.rank, self.size = arr.rank, arr.size
         self._nccl = dist.get_backend(group) == "nccl"
         self._flag = torch.zeros(1, dtype=torch.int32, device=blk.data.device)
-        mine = []
-        for buf in blk._bufs:
-            h = ctypes.create_string_buffer(64)
-            off = ctypes.c_int64()
-            _lib.check(_lib.lib().lope_ipc_export(ctypes.c_void_p(buf.data_ptr()), h, ctypes.byref(off)),
-                       "lope_ipc_export")
-            mine.append((bytes(h.raw), int(off.value)))
+        # Every step of the setup is agreed by all ranks: a rank that cannot export or
+        # map peer memory makes every rank raise (the caller then falls back to NCCL on
+        # all of them) instead of leaving the others waiting in a collective.
+        mine, why = [], None
+        try:
+            for buf in blk._bufs:
+                h = ctypes.create_string_buffer(64)
+                off = ctypes.c_int64()
+                _lib.check(_lib.lib().lope_ipc_export(ctypes.c_void_p(buf.data_ptr()), h, ctypes.byref(off)),
+                           "lope_ipc_export")
+                mine.append((bytes(h.raw), int(off.value)))
+        except Exception as e:          # pragma: no cover - depends on the allocator
+            mine, why = None, repr(e)
         allh = [None] * self.size
         dist.all_gather_object(allh, mine, group=group)
+        if any(x is None for x in allh):
+            raise RuntimeError(f"peer memory export failed on some rank ({why or 'another rank'})")
         prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
         self._opened = []
         self.peers = {}
+        ok = 1
         try:
             for who in sorted({prev, nxt}):
                 ptrs = []
@@ -783,9 +792,13 @@ class PeerSlabStepper:
                     self._opened.append(p.value)
                     ptrs.append(p.value)
                 self.peers[who] = ptrs
-        except Exception:
-            self.close()          # unmap whatever was mapped before the failure
-            raise
+        except Exception as e:          # pragma: no cover - depends on the node
+            ok, why = 0, repr(e)
+        flags = [None] * self.size
+        dist.all_gather_object(flags, ok, group=group)
+        if not all(flags):
+            self.close()                # unmap whatever was mapped
+            raise RuntimeError(f"peer memory mapping failed on some rank ({why or 'another rank'})")
         self.prev, self.next = prev, nxt
         d = arr.dim
         L = blk.layout
