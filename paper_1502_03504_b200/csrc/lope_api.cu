@@ -892,9 +892,14 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     pack[i].org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
                   (long long)(L->lo[2] + r0[2]) * L->stride[2];
   }
+  // enough blocks to fill the GPU a few times over; each block then walks many rows
+  // and planes (grid-stride) instead of one 128-point row segment per block
   unsigned gx = (unsigned)((ext[0] + 127) / 128);
-  unsigned gy = (unsigned)(ext[1] < 65535 ? ext[1] : 65535);
-  unsigned gz = (unsigned)(ext[2] < 65535 ? ext[2] : 65535);
+  const long long target = (long long)sm_count() * 16;
+  long long gyl = std::min<long long>(ext[1], std::max<long long>(1, std::min<long long>(32, target / gx)));
+  long long gzl = std::min<long long>(ext[2], std::max<long long>(1, target / ((long long)gx * gyl)));
+  unsigned gy = (unsigned)std::min<long long>(gyl, 65535);
+  unsigned gz = (unsigned)std::min<long long>(gzl, 65535);
   void* args[] = {pack.data(), &sc, &g};
   CUresult r = d.launchKernel(m->generic, gx, gy, gz, 128, 1, 1, 0, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_generic)");
