@@ -411,6 +411,29 @@ class CompiledKernel:
         return rs, is_
 
 
+_NVTX = None
+
+
+def _nvtx(name):
+    """NVTX range around a hot-path call when ``LOPE_NVTX=1`` (Nsight timelines: one
+    range per launch / step / exchange, the reference's event log as a trace)."""
+    global _NVTX
+    if _NVTX is None:
+        import os
+        _NVTX = os.environ.get("LOPE_NVTX", "0") not in ("0", "")
+    if not _NVTX:
+        return _NullRange()
+    return _torch().cuda.nvtx.range(name)
+
+
+class _NullRange:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def launch(kernel: CompiledKernel, arrays: Sequence[HaloArray], ranges=None,
            scalars: Optional[Dict[str, float]] = None, stream=None) -> None:
     """One ``do concurrent`` launch (runtime.py:541-618) over 1-based inclusive ``ranges``.
@@ -445,6 +468,11 @@ def launch(kernel: CompiledKernel, arrays: Sequence[HaloArray], ranges=None,
 
 
 def halo_transfer(arr: HaloArray, dims_mask: Optional[int] = None, stream=None) -> None:
+    with _nvtx(f"lope.halo_transfer {arr.name or ''}"):
+        _halo_transfer(arr, dims_mask, stream)
+
+
+def _halo_transfer(arr: HaloArray, dims_mask: Optional[int] = None, stream=None) -> None:
     """``HALO_TRANSFER(U, BC=CYCLIC)`` for one image (every neighbour is self)."""
     mask = (1 << arr.rank) - 1 if dims_mask is None else dims_mask
     _lib.check(_lib.lib().lope_halo_fill(ctypes.byref(arr.layout), ctypes.c_void_p(arr.data.data_ptr()),
@@ -454,6 +482,12 @@ def halo_transfer(arr: HaloArray, dims_mask: Optional[int] = None, stream=None) 
 
 def step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Optional[int] = None,
          stream=None) -> None:
+    with _nvtx(f"lope.step {kernel.ir.name}"):
+        _step(kernel, arr, scalars, wrap_mask, stream)
+
+
+def _step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Optional[int] = None,
+          stream=None) -> None:
     """Fused launch (full interior) + the following HALO_TRANSFER's local fill."""
     mask = (1 << arr.rank) - 1 if wrap_mask is None else wrap_mask
     tuner = kernel.tuner(arr, mask)
@@ -470,6 +504,11 @@ def step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Option
 
 
 def multi_step(kernel: CompiledKernel, arr: HaloArray, nsteps: int, scalars=None, stream=None) -> None:
+    with _nvtx(f"lope.multi_step {kernel.ir.name} x{nsteps}"):
+        _multi_step(kernel, arr, nsteps, scalars, stream)
+
+
+def _multi_step(kernel: CompiledKernel, arr: HaloArray, nsteps: int, scalars=None, stream=None) -> None:
     """``nsteps`` fused steps (every dim periodic) in as few launches as the kernel
     allows: rank-2 kernels on fields of at least a tile plus four halos advance four
     steps per launch in shared memory (``lope_step_multi``), bit-identical to
