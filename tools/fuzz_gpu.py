@@ -1,0 +1,161 @@
+"""GPU fuzz: random locally-oriented kernels through the product path vs the oracle.
+
+Random IR trees (+ - * / with constant, scalar and expression divisors, abs, sqrt,
+min, max, locals, pending-centre reads, one or two arrays), random rank 2/3, halos at
+least the footprint (sometimes wider, asymmetric), ragged or vector-aligned shapes,
+fp32 and fp64; ``iterate`` for a few steps (tiled or generic path, fused halo images,
+temporal blocking for small 2-D fields) compared bit for bit with the numpy
+restatement (fp64 == the reference's arithmetic).  Exits non-zero on a mismatch.
+
+    python tools/fuzz_gpu.py [cases] [seed]
+"""
+
+import pathlib
+import random
+import sys
+
+import numpy as np
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+
+from oracle import lope_oracle as O  # noqa: E402
+from paper_1502_03504_b200 import runtime as R  # noqa: E402
+from paper_1502_03504_b200.ir import KernelBuilder, fabs, fmax, fmin, fsqrt  # noqa: E402
+
+
+def rand_expr(rng, depth, rank, arrays, scalars, locals_):
+    if depth == 0 or rng.random() < 0.25:
+        kind = rng.randrange(5)
+        if kind <= 1:
+            a = rng.choice(arrays)
+            return a[tuple(rng.randrange(-2, 3) for _ in range(rank))]
+        if kind == 2:
+            return float(rng.choice([1, 2, 3, 0.5, 0.125, 1.5, 7, 0.1]))
+        if kind == 3 and scalars:
+            return rng.choice(scalars)
+        if locals_:
+            return rng.choice(locals_)
+        return arrays[0][(0,) * rank]
+    a = rand_expr(rng, depth - 1, rank, arrays, scalars, locals_)
+    b = rand_expr(rng, depth - 1, rank, arrays, scalars, locals_)
+    r = rng.random()
+    if r < 0.08:
+        return fabs(a)
+    if r < 0.13:
+        return fsqrt(fabs(a))
+    if r < 0.19:
+        return fmin(a, b)
+    if r < 0.25:
+        return fmax(a, b, rand_expr(rng, 0, rank, arrays, scalars, locals_))
+    if r < 0.33:
+        return a / rng.choice([3.0, 7.0, 25.0, 0.1, 2.0]) if rng.random() < 0.7 else a / (fabs(b) + 1.0)
+    if r < 0.40 and scalars:
+        return a / scalars[0]
+    op = rng.choice(["+", "-", "*"])
+    return a + b if op == "+" else (a - b if op == "-" else a * b)
+
+
+def make_kernel(rng, rank):
+    kb = KernelBuilder("fz", rank)
+    narr = 2 if rng.random() < 0.2 else 1
+    arrays = [kb.array(n) for n in ("u", "v")[:narr]]
+    scalars = [kb.scalar("c")] if rng.random() < 0.5 else []
+    locals_ = []
+    if rng.random() < 0.3:
+        locals_.append(kb.let("t", rand_expr(rng, 2, rank, arrays, scalars, [])))
+    kb.store(arrays[0], rand_expr(rng, 3, rank, arrays, scalars, locals_))
+    if narr == 2 and rng.random() < 0.5:
+        kb.store(arrays[1], rand_expr(rng, 2, rank, arrays, scalars, locals_) + arrays[0][(0,) * rank])
+    return kb.build()
+
+
+def run_case(rng, case):
+    rank = 2 if rng.random() < 0.6 else 3
+    try:
+        kir = make_kernel(rng, rank)
+    except ValueError:          # E103-style programs the checker rejects
+        return None
+    dt = rng.choice(["float32", "float64"])
+    npdt = np.float32 if dt == "float32" else np.float64
+    vx = 4 if dt == "float32" else 2
+    fps = [kir.footprints[a].dims for a in kir.array_params]
+    lo = [max(f[d][0] for f in fps) + (rng.randrange(2) if rng.random() < 0.3 else 0) for d in range(rank)]
+    hi = [max(f[d][1] for f in fps) + (rng.randrange(2) if rng.random() < 0.3 else 0) for d in range(rank)]
+    if rank == 2:
+        mx = rng.choice([rng.randrange(9, 90) * vx, rng.randrange(20, 300), 288, 320])
+        shape = (mx, rng.randrange(max(lo[1] + hi[1], 5), 80))
+    else:
+        shape = (rng.randrange(9, 40) * vx, rng.randrange(max(lo[1] + hi[1], 4), 30),
+                 rng.randrange(max(lo[2] + hi[2], 3), 20))
+    if any(s < l + h or s < 1 for s, l, h in zip(shape, lo, hi)):
+        return None
+    sc = {"c": rng.choice([0.25, 3.0, -1.5, 7.0])} if "c" in kir.scalar_params else None
+    steps = rng.randrange(1, 6)
+    fields = [O.hash_field(shape, 100 + case + 7 * i, npdt) for i in range(len(kir.array_params))]
+    k = R.CompiledKernel(kir, dt)
+    arrs = []
+    for f in fields:
+        a = R.HaloArray(shape, lo, hi, dt)
+        a.set_interior(f)
+        arrs.append(a)
+    if len(arrs) == 1:
+        R.iterate(k, arrs[0], steps, sc)
+        got = [arrs[0].get_interior()]
+        want = fields[0]
+        with np.errstate(all="ignore"):
+            for _ in range(steps):
+                want = np.broadcast_to(O.periodic_apply(want, kir, sc, npdt), shape).astype(npdt)
+        want = [want]
+    else:
+        # two arrays: one launch per step after a periodic halo fill of both (the oracle
+        # works on the dense periodic fields)
+        cur = list(fields)
+        for _ in range(steps):
+            for a in arrs:
+                R.halo_transfer(a)
+            R.launch(k, arrs, None, sc)
+            with np.errstate(all="ignore"):
+                cur = _oracle_multi(kir, cur, sc, npdt)
+        got = [a.get_interior() for a in arrs]
+        want = cur
+    for g_, w_ in zip(got, want):
+        if not O.equal_bits(g_, w_):
+            return (kir, dt, shape, lo, hi, steps, O.first_mismatch(g_, w_))
+    return True
+
+
+def _oracle_multi(kir, fields, sc, npdt):
+    axes = tuple(range(fields[0].ndim))
+    names = list(kir.array_params)
+
+    def read(name, offsets):
+        f = fields[names.index(name)]
+        if all(o == 0 for o in offsets):
+            return f.copy()
+        return np.roll(f, shift=tuple(-o for o in offsets), axis=axes)
+
+    pending = O.run_body(kir, read, sc, npdt)
+    return [np.broadcast_to(np.asarray(pending[n], dtype=npdt), fields[0].shape).copy() if n in pending
+            else fields[i] for i, n in enumerate(names)]
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    rng = random.Random(seed)
+    ran = bad = 0
+    for c in range(cases):
+        r = run_case(rng, c)
+        if r is None:
+            continue
+        ran += 1
+        if r is not True:
+            bad += 1
+            kir, dt, shape, lo, hi, steps, mm = r
+            print("MISMATCH", dt, shape, lo, hi, steps, mm, kir, flush=True)
+    print(f"fuzz: {ran} cases, {bad} mismatches", flush=True)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
