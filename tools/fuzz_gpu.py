@@ -7,7 +7,9 @@ fp32 and fp64; ``iterate`` for a few steps (tiled or generic path, fused halo im
 temporal blocking for small 2-D fields) compared bit for bit with the numpy
 restatement (fp64 == the reference's arithmetic).  Exits non-zero on a mismatch.
 
-    python tools/fuzz_gpu.py [cases] [seed]
+    python tools/fuzz_gpu.py [cases] [seed] [--decomp]
+
+``--decomp``: slab / fused-peer / grid decompositions on one GPU vs the undecomposed run.
 """
 
 import pathlib
@@ -124,6 +126,56 @@ def run_case(rng, case):
     return True
 
 
+def run_decomp_case(rng, case):
+    """One-array kernel, random slab count / grid: MultiSlab, PeerMultiSlab and MultiGrid
+    against the undecomposed run (the multi-GPU orchestration with in-process images)."""
+    from paper_1502_03504_b200 import dist as D
+    rank = 2 if rng.random() < 0.6 else 3
+    try:
+        kb_kir = make_kernel(rng, rank)
+    except ValueError:
+        return None
+    if len(kb_kir.array_params) != 1:
+        return None
+    kir = kb_kir
+    dt = rng.choice(["float32", "float64"])
+    npdt = np.float32 if dt == "float32" else np.float64
+    vx = 4 if dt == "float32" else 2
+    fp = kir.footprints[kir.array_params[0]].dims
+    lo = [n for n, _ in fp]
+    hi = [p for _, p in fp]
+    P = rng.choice([2, 3, 4])
+    if rank == 2:
+        shape = (rng.randrange(9, 60) * vx, P * rng.randrange(max(lo[1] + hi[1], 3), 20))
+    else:
+        shape = (rng.randrange(9, 30) * vx, rng.randrange(max(lo[1] + hi[1], 4), 24),
+                 P * rng.randrange(max(lo[2] + hi[2], 3), 10))
+    if any(s < l + h for s, l, h in zip(shape, lo, hi)):
+        return None
+    sc = {"c": rng.choice([0.25, 3.0, -1.5])} if "c" in kir.scalar_params else None
+    steps = rng.randrange(2, 5)
+    field = O.hash_field(shape, 500 + case, npdt)
+    k = R.CompiledKernel(kir, dt)
+    base = R.HaloArray(shape, lo, hi, dt)
+    base.set_interior(field)
+    R.iterate(k, base, steps, sc)
+    want = base.get_interior()
+    runs = [("slab", D.MultiSlab(k, shape, lo, hi, dt, P, sc)),
+            ("peer", D.PeerMultiSlab(k, shape, lo, hi, dt, P, sc))]
+    splits = [1] * rank
+    splits[rng.randrange(rank)] = P
+    if all(s % q == 0 for s, q in zip(shape, splits)) and all(
+            s // q >= l + h or q == 1 for s, q, l, h in zip(shape, splits, lo, hi)):
+        runs.append(("grid", D.MultiGrid(k, D.CartGrid(shape, splits, lo, hi), dt, sc)))
+    for name, ms in runs:
+        ms.set_global(field)
+        ms.iterate(steps)
+        got = ms.get_global()
+        if not O.equal_bits(got, want):
+            return (kir, dt, shape, lo, hi, steps, (name, P, splits, O.first_mismatch(got, want)))
+    return True
+
+
 def _oracle_multi(kir, fields, sc, npdt):
     axes = tuple(range(fields[0].ndim))
     names = list(kir.array_params)
@@ -140,12 +192,14 @@ def _oracle_multi(kir, fields, sc, npdt):
 
 
 def main():
-    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    cases = int(args[0]) if len(args) > 0 else 200
+    seed = int(args[1]) if len(args) > 1 else 1
     rng = random.Random(seed)
+    decomp = "--decomp" in sys.argv
     ran = bad = 0
     for c in range(cases):
-        r = run_case(rng, c)
+        r = run_decomp_case(rng, c) if decomp else run_case(rng, c)
         if r is None:
             continue
         ran += 1
