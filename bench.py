@@ -494,6 +494,10 @@ def main():
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
     wl = WORKLOADS[args.workload]
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != ws_env:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws_env}; launch N>1 with torchrun "
+            f"(--nproc-per-node N); reporting n_gpus={ws_env}")
     if args.impl == "reference":
         run_reference_arm(args, wl)
     else:
