@@ -405,12 +405,15 @@ TileCfg pick_tile(const lope::Kir& k, int dtype) {
   c.mb = 1;
   c.ns = 32;
   // producer: in-band (warp 0 lane 0) for 3-D, a dedicated 17th warp for 2-D
-  // (measured on B200: lap3d7 1024^3 1.76 vs 1.98 ms; ninept2d 16384^2 0.35 vs 0.49 ms)
+  // (measured on B200: lap3d7 1024^3 1.76 vs 1.98 ms; ninept2d 16384^2 0.35 vs 0.49 ms).
+  // This is the untuned default; the plan tuner may pick a dedicated producer with
+  // short z-chunks for 3-D (tune_candidates).
   c.pw = k.rank == 3 ? 0 : 1;
   if (dtype == LOPE_F64) {
     // fp64 lanes hold 2 values: two warps side by side keep the TMA box 128+ columns
     // wide (fewer partial lines); lap3d7 fp64 1024^2x512: 1.57 ms = 5.5 TB/s.  The 5x5
-    // box is FP64-latency bound and prefers 4 rows per lane in one warp column.
+    // box (24 dependent adds per point) prefers 4 rows per lane in one warp column:
+    // more independent chains per lane.
     c.bxw = 2; c.wy = 8; c.ry = 2; c.pw = 0;
     const int wide = (k.fn[0][0] + k.fp[0][0] + 2) * (c.ry + k.fn[0][1] + k.fp[0][1]) * 2;
     if (wide > 64) { c.bxw = 1; c.wy = 16; c.ry = 4; }
