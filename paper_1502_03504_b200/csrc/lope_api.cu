@@ -303,6 +303,8 @@ struct DevMod {
   CUfunction tiled = nullptr;
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
   int tiled_local = 0;                  // local memory (spills) per thread of the tiled kernel
+  CUfunction tiledm = nullptr;          // multi-array tiled kernel, variant 0 only
+  int tm_smem = 0, tm_threads = 0, tm_boxx = 0, tm_boxy = 0, tm_blocks = 0;
   CUfunction tblock = nullptr;          // temporal blocking (rank 2), variant 0 only
   int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0, tb_threads = 0;
 };
@@ -473,6 +475,37 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.pw << ", " << c.sh << ", " << c.nb << ">(&map, a, sc, g);\n"
       << "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   }
+  if (with_tblock && k.rank >= 2 && k.arrays.size() >= 2 && k.arrays.size() <= 4) {
+    // several arrays: one TMA box per array per plane (lope_tiled_multi_impl); ring as
+    // deep as fits next to NA boxes per stage
+    const int na = (int)k.arrays.size();
+    const int ry = k.rank == 3 ? 1 : 2;
+    int ns = 12;
+    auto fits = [&](int n) {
+      const int sz = K->dtype == LOPE_F32 ? 4 : 8, vx = 16 / sz;
+      int un0 = 0, up0 = 0, un1 = 0, up1 = 0, un2 = 0, up2 = 0;
+      for (int a = 0; a < na; ++a) {
+        un0 = std::max(un0, k.fn[a][0]); up0 = std::max(up0, k.fp[a][0]);
+        un1 = std::max(un1, k.fn[a][1]); up1 = std::max(up1, k.fp[a][1]);
+        un2 = std::max(un2, k.fn[a][2]); up2 = std::max(up2, k.fp[a][2]);
+      }
+      const int boxx = ((un0 + vx - 1) / vx) * vx + 32 * vx + ((up0 + vx - 1) / vx) * vx;
+      const int boxy = 16 * ry + un1 + up1;
+      if (boxx > 256 || boxy > 256) return false;
+      const int box = ((boxx * boxy * sz + 127) / 128) * 128;
+      return n >= un2 + up2 + 2 && n * na * box + 16 * n <= 225 * 1024;
+    };
+    while (ns > 2 && !fits(ns)) --ns;
+    if (fits(ns)) {
+      s << "typedef LopeTiledMCfg<LopeBody, LT, 1, 16, " << ry << ", " << ns << "> LopeMCfg;\n";
+      s << "extern \"C\" __constant__ int lope_tiledm_info[4] = {LopeMCfg::SMEM_BYTES, LopeMCfg::THREADS, "
+           "LopeMCfg::BOXX, LopeMCfg::BOXY};\n";
+      s << "extern \"C\" __global__ void __launch_bounds__(LopeMCfg::THREADS, 1) lope_tiled_multi("
+           "const __grid_constant__ LopeTmapPack<" << na << "> maps, const __grid_constant__ LopeArrPackT<LT, "
+        << na << "> arrs, const LopeScal<LT> sc, const LopeGeom g) {\n"
+        << "  lope_tiled_multi_impl<LopeBody, LT, 1, 16, " << ry << ", " << ns << ">(&maps, arrs, sc, g);\n}\n";
+    }
+  }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1 && k.fn[0][0] <= 4 && k.fp[0][0] <= 4) {
     // 256 x 28 fp32 tiles: 1024^2 splits into 4 x 37 = 148 CTAs, one per SM (config 1);
     // 8 steps per launch for one-cell footprints, 4 for wider ones (the recomputed
@@ -593,6 +626,25 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     int lb = 0;
     if (d.funcGetAttribute(&lb, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, m.tiled) == CUDA_SUCCESS) m.tiled_local = lb;
   }
+  if (d.moduleGetFunction(&m.tiledm, m.mod, "lope_tiled_multi") == CUDA_SUCCESS) {
+    CUdeviceptr gp;
+    size_t gsz;
+    r = d.moduleGetGlobal(&gp, &gsz, m.mod, "lope_tiledm_info");
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetGlobal(lope_tiledm_info)");
+    int info[4];
+    CUDA_TRY(cudaMemcpy(info, (const void*)gp, sizeof info, cudaMemcpyDeviceToHost));
+    m.tm_smem = info[0];
+    m.tm_threads = info[1];
+    m.tm_boxx = info[2];
+    m.tm_boxy = info[3];
+    int nb = 0;
+    if (d.funcSetAttribute(m.tiledm, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tm_smem) != CUDA_SUCCESS ||
+        d.occupancy(&nb, m.tiledm, m.tm_threads, m.tm_smem) != CUDA_SUCCESS || nb < 1)
+      m.tiledm = nullptr;
+    m.tm_blocks = nb;
+  } else {
+    m.tiledm = nullptr;
+  }
   if (d.moduleGetFunction(&m.tblock, m.mod, "lope_tblock") == CUDA_SUCCESS) {
     CUdeviceptr gp;
     size_t gsz;
@@ -697,12 +749,18 @@ bool tmap_flat() {
   return v;
 }
 
+int encode_tmap_box(const lope_layout* L, const void* base, int boxx, int boxy, CUtensorMap* map);
+
 int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtensorMap* map) {
+  return encode_tmap_box(L, base, m.boxx, m.boxy, map);
+}
+
+int encode_tmap_box(const lope_layout* L, const void* base, int boxx, int boxy, CUtensorMap* map) {
   if (tmap_flat()) {
     // planes stacked as rows: one 2-D map over padded1*padded2 rows
     cuuint64_t dims2[2] = {(cuuint64_t)L->stride[1], (cuuint64_t)(L->padded[1] * L->padded[2])};
     cuuint64_t strides2[1] = {(cuuint64_t)(L->stride[1] * L->elem_bytes)};
-    cuuint32_t box2[2] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy};
+    cuuint32_t box2[2] = {(cuuint32_t)boxx, (cuuint32_t)boxy};
     cuuint32_t estr2[2] = {1, 1};
     CUresult r2 = drv().tensorMapEncodeTiled(
         map, L->dtype == LOPE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
@@ -713,7 +771,7 @@ int encode_tmap(const lope_layout* L, const void* base, const DevMod& m, CUtenso
   }
   cuuint64_t dims[3] = {(cuuint64_t)L->stride[1], (cuuint64_t)L->padded[1], (cuuint64_t)L->padded[2]};
   cuuint64_t strides[2] = {(cuuint64_t)(L->stride[1] * L->elem_bytes), (cuuint64_t)(L->stride[2] * L->elem_bytes)};
-  cuuint32_t box[3] = {(cuuint32_t)m.boxx, (cuuint32_t)m.boxy, 1};
+  cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = drv().tensorMapEncodeTiled(
       map, L->dtype == LOPE_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
@@ -885,6 +943,62 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     g_launches++;
     return 0;
   }
+  // several arrays with one layout: the multi-array tiled kernel
+  const int na = (int)k.arrays.size();
+  bool same = na >= 2 && na <= 4 && m->tiledm && geom_ok && !std::getenv("LOPE_FORCE_GENERIC");
+  for (int a = 1; same && a < na; ++a) {
+    const lope_layout& A = layouts[a];
+    const lope_layout& B = layouts[0];
+    for (int d = 0; d < 3; ++d)
+      same = same && A.interior[d] == B.interior[d] && A.lo[d] == B.lo[d] && A.hi[d] == B.hi[d] &&
+             A.stride[d] == B.stride[d];
+    same = same && A.base == B.base && A.rank == B.rank;
+  }
+  for (int a = 0; same && a < na; ++a) same = in[a] != nullptr;
+  for (size_t q = 0; same && q < k.stored.size(); ++q) same = out && out[k.stored[q]] != nullptr;
+  same = same && wrap == 0;      // the multi-array kernel stores no periodic images
+  if (same) {
+    const lope_layout* L = &layouts[0];
+    std::vector<CUtensorMap> maps(na);
+    for (int a = 0; a < na; ++a)
+      if (int e = encode_tmap_box(L, in[a], m->tm_boxx, m->tm_boxy, &maps[a])) return e;
+    std::vector<HArr<T>> pk(na);
+    int un0 = 0;
+    for (int a = 0; a < na; ++a) {
+      pk[a].in = (const T*)in[a];
+      pk[a].out = out ? (T*)out[a] : nullptr;
+      pk[a].s1 = L->stride[1];
+      pk[a].s2 = L->stride[2];
+      pk[a].org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+                  (long long)(L->lo[2] + r0[2]) * L->stride[2];
+      un0 = std::max(un0, k.fn[a][0]);
+    }
+    const int padx = ((un0 + vx - 1) / vx) * vx;
+    g.box0 = (int)(L->base + L->lo[0] + r0[0] - padx);
+    const int ry = k.rank == 3 ? 1 : 2;
+    long long ntx = (ext[0] + 32 * vx - 1) / (32 * vx);
+    long long nty = (ext[1] + 16 * ry - 1) / (16 * ry);
+    long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
+    long long units = ntx * nty * nzc;
+    if (units >= (1LL << 31)) return fail(108, "launch range too large for the tiled path");
+    long long grid = (long long)m->tm_blocks * sm_count();
+    {
+      long long period = ntx * nty, best = grid;
+      for (long long gg = grid; gg > 1 && gg > grid - 32; --gg) {
+        long long a0 = gg, b0 = period;
+        while (b0) { long long t = a0 % b0; a0 = b0; b0 = t; }
+        if (a0 == 1) { best = gg; break; }
+      }
+      grid = best;
+    }
+    if (grid > units) grid = units;
+    if (grid < 1) grid = 1;
+    void* args[] = {maps.data(), pk.data(), &sc, &g};
+    CUresult r = launch_ex(m->tiledm, (unsigned)grid, (unsigned)m->tm_threads, m->tm_smem, st, args);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tiled_multi)");
+    g_launches++;
+    return 0;
+  }
   std::vector<HArr<T>> pack(k.arrays.size());
   for (size_t i = 0; i < k.arrays.size(); ++i) {
     const lope_layout* L = &layouts[i];
@@ -1016,7 +1130,9 @@ int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kerne
   if (!err.empty()) return fail(104, "kernel IR rejected: %s", err.c_str());
   K->dtype = dtype;
   if (int e = add_variant(K.get(), pick_tile(K->ir, dtype))) return e;
-  K->describe_path = K->tiled_ok() ? "tiled_tma" : "generic";
+  K->describe_path = K->tiled_ok() ? "tiled_tma"
+                     : (K->variants[0].source.find("lope_tiled_multi(") != std::string::npos ? "tiled_tma_multi"
+                                                                                           : "generic");
   *out = K.release();
   return 0;
 }

@@ -5,6 +5,7 @@
 // contract into FMA), constants are exact hex literals converted to T once
 // (np.float32(value) semantics), and a centre read of an array stored earlier
 // in the body reads the pending value (ir.py:278-280).
+#include <algorithm>
 #include "lope_codegen.h"
 
 #include <cmath>
@@ -326,6 +327,17 @@ std::string emit_body(const Kir& k) {
   for (int d = 0; d < 3; ++d) {
     o << "  static constexpr int FN" << dn[d] << " = " << k.fn[0][d] << ";\n";
     o << "  static constexpr int FP" << dn[d] << " = " << k.fp[0][d] << ";\n";
+  }
+  // union of every array's footprint (the multi-array tiled kernel stages one box per
+  // array with these halos)
+  for (int d = 0; d < 3; ++d) {
+    int un = 0, up = 0;
+    for (size_t a = 0; a < k.arrays.size(); ++a) {
+      un = std::max(un, k.fn[a][d]);
+      up = std::max(up, k.fp[a][d]);
+    }
+    o << "  static constexpr int UFN" << dn[d] << " = " << un << ";\n";
+    o << "  static constexpr int UFP" << dn[d] << " = " << up << ";\n";
   }
   // ZSTAR: every read of array 0 off the centre plane is at x = y = 0 (past planes can
   // live in registers in the tiled kernel)

@@ -975,3 +975,209 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
     __syncthreads();
   }
 }
+
+// --------------------------------------------------------------------------
+// Multi-array tiled path (rank 2/3, 2..4 array parameters with identical layouts).
+//
+// The single-array kernel's structure with one TMA box per array per plane in each
+// ring stage (one mbarrier, NA boxes of bytes), the union of the arrays' footprints as
+// the box halo, all NZW planes of a unit held in the ring (no z history) and the
+// producer in warp 0 lane 0.  Used by plain launches (lope_launch), which store the
+// interior only.
+
+template <class T, int NA, int NZW, int NR, int NXW, int FN0, int FN1, int FZN>
+struct LopeWinReaderM {
+  const T* win;    // [NA][NZW][NR][NXW]
+  int r, v;
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ T at() const {
+    return win[((A * NZW + DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0)];
+  }
+};
+
+template <class Body, class T, int WX, int WY, int RY, int NS>
+struct LopeTiledMCfg {
+  static constexpr int NA = Body::NARR;
+  static constexpr int VX = 16 / (int)sizeof(T);
+  static constexpr int BX = 32 * VX * WX;
+  static constexpr int BY = WY * RY;
+  static constexpr int PADX = ((Body::UFN0 + VX - 1) / VX) * VX;
+  static constexpr int BOXX = PADX + BX + ((Body::UFP0 + VX - 1) / VX) * VX;
+  static constexpr int BOXY = BY + Body::UFN1 + Body::UFP1;
+  static constexpr int NZW = Body::UFN2 + Body::UFP2 + 1;
+  static constexpr int BOX_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
+  static constexpr int STAGE_BYTES = NA * BOX_BYTES;
+  static constexpr int TX_BYTES = NA * BOXX * BOXY * (int)sizeof(T);
+  static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
+  static constexpr int NCW = WX * WY;
+  static constexpr int THREADS = 32 * NCW;
+  static constexpr int NR = RY + Body::UFN1 + Body::UFP1;
+  static constexpr int NXW = VX + Body::UFN0 + Body::UFP0;
+};
+
+template <int NA> struct LopeTmapPack { LopeTmap m[NA]; };
+template <class T, int NA> struct LopeArrPackT { LopeArr<T> a[NA]; };
+
+template <class Body, class T, int WX, int WY, int RY, int NS>
+__device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::NARR>* maps,
+                                                      const LopeArrPackT<T, Body::NARR>& arrs,
+                                                      const LopeScal<T>& sc, const LopeGeom& g) {
+  typedef LopeTiledMCfg<Body, T, WX, WY, RY, NS> C;
+  typedef typename LopeVec<T>::V V;
+  constexpr int NA = C::NA, VX = C::VX, NZW = C::NZW, NR = C::NR, NXW = C::NXW;
+  constexpr int FN0 = Body::UFN0, FP0 = Body::UFP0, FN1 = Body::UFN1, FP1 = Body::UFP1;
+  constexpr int FZN = Body::UFN2;
+  static_assert(NS >= NZW + 1, "ring must hold a unit's planes in use plus one prefetch slot");
+  static_assert(C::BOXX <= 256 && C::BOXY <= 256, "TMA box dimensions are limited to 256");
+  extern __shared__ __align__(128) unsigned char lope_smem[];
+  lope_u64* full = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
+  lope_u64* empty = full + NS;
+  const int ntx = (g.ext[0] + C::BX - 1) / C::BX;
+  const int nty = (g.ext[1] + C::BY - 1) / C::BY;
+  const int zc = g.zchunk;
+  const int nzc = (g.ext[2] + zc - 1) / zc;
+  const int nunits = ntx * nty * nzc;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) lope_tma_prefetch_desc(&maps->m[a]);
+    for (int s = 0; s < NS; ++s) {
+      lope_mbar_init(&full[s], 1);
+      lope_mbar_init(&empty[s], C::NCW);
+    }
+    lope_fence_init();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+
+  LopeUnitWalk pw;
+  int p_u = blockIdx.x, p_pl = 0, p_nl = 0, p_bx = 0, p_by = 0, p_z = 0;
+  lope_u32 p_L = 0;
+  const int oy = g.lo[1] + g.r0[1] - FN1;
+  const int oz = g.lo[2] + g.r0[2] - FZN;
+  if (warp == 0 && lane == 0) {
+    pw.init(blockIdx.x, gridDim.x, ntx, nty, nzc);
+    if (p_u < nunits) {
+      const int z0 = pw.zi * zc;
+      p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+      p_bx = g.box0 + pw.tx * C::BX;
+      p_by = oy + pw.ty() * C::BY;
+      p_z = oz + z0;
+    }
+  }
+  auto produce = [&](lope_u32 limit) {
+    while (p_L < limit && p_u < nunits) {
+      const lope_u32 slot = p_L % NS;
+      if (p_L >= (lope_u32)NS) lope_mbar_wait(&empty[slot], ((p_L / NS) - 1) & 1);
+      lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        unsigned char* dst = lope_smem + slot * C::STAGE_BYTES + a * C::BOX_BYTES;
+        if (g.p1 > 0)
+          lope_tma_load_2d(dst, &maps->m[a], &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
+        else
+          lope_tma_load_3d(dst, &maps->m[a], &full[slot], p_bx, p_by, p_z + p_pl);
+      }
+      ++p_L;
+      if (++p_pl == p_nl) {
+        p_pl = 0;
+        p_u += gridDim.x;
+        pw.next();
+        if (p_u < nunits) {
+          const int z0 = pw.zi * zc;
+          p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+          p_bx = g.box0 + pw.tx * C::BX;
+          p_by = oy + pw.ty() * C::BY;
+          p_z = oz + z0;
+        }
+      }
+    }
+  };
+
+  const int wx = warp % WX;
+  const int wy = warp / WX;
+  const int cx = (wx * 32 + lane) * VX;
+  const int row0 = wy * RY;
+  const lope_i64 s1 = arrs.a[0].s1, s2 = arrs.a[0].s2;
+  const int soff = (row0 * C::BOXX + C::PADX + cx);
+  LopeUnitWalk w;
+  w.init(blockIdx.x, gridDim.x, ntx, nty, nzc);
+  lope_u32 lbase = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
+    const int z0 = w.zi * zc;
+    const int nz = min(zc, g.ext[2] - z0);
+    const int x = w.tx * C::BX + cx;
+    const int ybase = w.ty() * C::BY + row0;
+    const bool xok = x < g.ext[0];
+    const int nrow = min(RY, g.ext[1] - ybase);
+    const lope_i64 rowoff = x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
+    for (int pz = 0; pz < nz; ++pz) {
+      if (warp == 0) {
+        if (lane == 0) produce(lbase + pz + NS);
+        __syncwarp();
+      }
+      const T* sp[NZW];
+#pragma unroll
+      for (int k = 0; k < NZW; ++k) {
+        const lope_u32 L = lbase + pz + k;
+        sp[k] = reinterpret_cast<const T*>(lope_smem + (L % NS) * C::STAGE_BYTES) + soff;
+        lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+      }
+      T win[NA][NZW][NR][NXW];
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int k = 0; k < NZW; ++k)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            const T* rp = reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(sp[k]) +
+                                                     a * C::BOX_BYTES) + q * C::BOXX;
+            const V vv = *reinterpret_cast<const V*>(rp);
+            const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) win[a][k][q][FN0 + e] = ve[e];
+#pragma unroll
+            for (int e = 1; e <= FN0; ++e) win[a][k][q][FN0 - e] = rp[-e];
+#pragma unroll
+            for (int e = 0; e < FP0; ++e) win[a][k][q][FN0 + VX + e] = rp[VX + e];
+          }
+      T vals[RY][VX][Body::NSTORE > 0 ? Body::NSTORE : 1];
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int v = 0; v < VX; ++v) {
+          LopeWinReaderM<T, NA, NZW, NR, NXW, FN0, FN1, FZN> rd;
+          rd.win = &win[0][0][0][0];
+          rd.r = r;
+          rd.v = v;
+          bool slow = false;
+          Body::template eval<T, false>(rd, sc.v, vals[r][v], slow);
+        }
+      __syncwarp();
+      if (lane == 0) {
+        lope_mbar_arrive(&empty[(lbase + pz) % NS]);
+        if (pz == nz - 1)
+          for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
+      }
+      if (!xok || nrow <= 0) continue;
+      // plain launches only (lope_launch): stored arrays get their interior points; the
+      // periodic images are refreshed by the next HALO_TRANSFER (lope_halo_fill)
+#pragma unroll
+      for (int q = 0; q < Body::NSTORE; ++q) {
+        T* ob = arrs.a[Body::stored(q)].out + arrs.a[Body::stored(q)].org + rowoff + (lope_i64)pz * s2;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          if (r >= nrow) continue;
+          V o;
+          T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e][q];
+          *reinterpret_cast<V*>(ob + (lope_i64)r * s1) = o;
+        }
+      }
+    }
+    lbase += nz + NZW - 1;
+  }
+}
