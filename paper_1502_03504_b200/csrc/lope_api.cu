@@ -497,13 +497,16 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
     };
     while (ns > 2 && !fits(ns)) --ns;
     if (fits(ns)) {
-      s << "typedef LopeTiledMCfg<LopeBody, LT, 1, 16, " << ry << ", " << ns << "> LopeMCfg;\n";
+      int mpw = k.rank == 2 ? 1 : 0;   // 2-D: a dedicated producer warp (as for one array)
+      if (const char* e = std::getenv("LOPE_MULTI_PW")) mpw = std::atoi(e) ? 1 : 0;
+      s << "typedef LopeTiledMCfg<LopeBody, LT, 1, 16, " << ry << ", " << ns << ", " << mpw << "> LopeMCfg;\n";
       s << "extern \"C\" __constant__ int lope_tiledm_info[4] = {LopeMCfg::SMEM_BYTES, LopeMCfg::THREADS, "
            "LopeMCfg::BOXX, LopeMCfg::BOXY};\n";
       s << "extern \"C\" __global__ void __launch_bounds__(LopeMCfg::THREADS, 1) lope_tiled_multi("
            "const __grid_constant__ LopeTmapPack<" << na << "> maps, const __grid_constant__ LopeArrPackT<LT, "
         << na << "> arrs, const LopeScal<LT> sc, const LopeGeom g) {\n"
-        << "  lope_tiled_multi_impl<LopeBody, LT, 1, 16, " << ry << ", " << ns << ">(&maps, arrs, sc, g);\n}\n";
+        << "  lope_tiled_multi_impl<LopeBody, LT, 1, 16, " << ry << ", " << ns << ", " << mpw
+        << ">(&maps, arrs, sc, g);\n}\n";
     }
   }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1 && k.fn[0][0] <= 4 && k.fp[0][0] <= 4) {

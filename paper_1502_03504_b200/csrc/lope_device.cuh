@@ -995,7 +995,7 @@ struct LopeWinReaderM {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0>
 struct LopeTiledMCfg {
   static constexpr int NA = Body::NARR;
   static constexpr int VX = 16 / (int)sizeof(T);
@@ -1010,7 +1010,7 @@ struct LopeTiledMCfg {
   static constexpr int TX_BYTES = NA * BOXX * BOXY * (int)sizeof(T);
   static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
   static constexpr int NCW = WX * WY;
-  static constexpr int THREADS = 32 * NCW;
+  static constexpr int THREADS = 32 * (NCW + PW);
   static constexpr int NR = RY + Body::UFN1 + Body::UFP1;
   static constexpr int NXW = VX + Body::UFN0 + Body::UFP0;
 };
@@ -1018,11 +1018,11 @@ struct LopeTiledMCfg {
 template <int NA> struct LopeTmapPack { LopeTmap m[NA]; };
 template <class T, int NA> struct LopeArrPackT { LopeArr<T> a[NA]; };
 
-template <class Body, class T, int WX, int WY, int RY, int NS>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0>
 __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::NARR>* maps,
                                                       const LopeArrPackT<T, Body::NARR>& arrs,
                                                       const LopeScal<T>& sc, const LopeGeom& g) {
-  typedef LopeTiledMCfg<Body, T, WX, WY, RY, NS> C;
+  typedef LopeTiledMCfg<Body, T, WX, WY, RY, NS, PW> C;
   typedef typename LopeVec<T>::V V;
   constexpr int NA = C::NA, VX = C::VX, NZW = C::NZW, NR = C::NR, NXW = C::NXW;
   constexpr int FN0 = Body::UFN0, FP0 = Body::UFP0, FN1 = Body::UFN1, FP1 = Body::UFP1;
@@ -1057,7 +1057,8 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
   lope_u32 p_L = 0;
   const int oy = g.lo[1] + g.r0[1] - FN1;
   const int oz = g.lo[2] + g.r0[2] - FZN;
-  if (warp == 0 && lane == 0) {
+  const int pwarp = PW ? C::NCW : 0;
+  if (warp == pwarp && lane == 0) {
     pw.init(blockIdx.x, gridDim.x, ntx, nty, nzc);
     if (p_u < nunits) {
       const int z0 = pw.zi * zc;
@@ -1096,6 +1097,10 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
     }
   };
 
+  if (PW && warp == C::NCW) {
+    if (lane == 0) produce(0xffffffffu);
+    return;
+  }
   const int wx = warp % WX;
   const int wy = warp / WX;
   const int cx = (wx * 32 + lane) * VX;
@@ -1114,7 +1119,7 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
     const int nrow = min(RY, g.ext[1] - ybase);
     const lope_i64 rowoff = x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
     for (int pz = 0; pz < nz; ++pz) {
-      if (warp == 0) {
+      if (!PW && warp == 0) {
         if (lane == 0) produce(lbase + pz + NS);
         __syncwarp();
       }
