@@ -161,3 +161,32 @@ def test_plan_watchdog_falls_back_only_on_the_slow_mode():
     t._check_window()
     assert not t.monitoring and calls == [(0, 64, 0)]
     assert t.report["fallback"]["to"] == [0, 64, 0]
+
+
+def test_boundary_rejects_bad_calls_with_reference_codes():
+    """Argument checks of the C ABI run before any device work (so they are testable on
+    the CPU) and come back as the reference's E-codes."""
+    import ctypes
+    L = _lib.lib()
+    h = _lib.compile_kernel(serialize(stencils.lap3d7()), "f32")
+    lay = _lib.make_layout(3, "f32", (64, 32, 16), (1, 1, 1), (1, 1, 1))
+    thin = _lib.make_layout(3, "f32", (64, 32, 16), (0, 1, 1), (1, 1, 1))
+    lay64 = _lib.make_layout(3, "f64", (64, 32, 16), (1, 1, 1), (1, 1, 1))
+    rs, is_ = (ctypes.c_double * 1)(), (ctypes.c_int64 * 1)()
+    A, B = ctypes.c_void_p(0x1000), ctypes.c_void_p(0x2000)
+
+    assert L.lope_step(h, ctypes.byref(lay), A, A, rs, is_, 7, None) == 108            # in == out
+    assert L.lope_step(h, ctypes.byref(thin), A, B, rs, is_, 7, None) == 102           # footprint > halo
+    assert L.lope_step(h, ctypes.byref(lay64), A, B, rs, is_, 7, None) == 108          # dtype mismatch
+    assert L.lope_step(h, ctypes.byref(lay), None, B, rs, is_, 7, None) == 202         # unallocated
+    assert L.lope_step_planes(h, ctypes.byref(lay), A, B, 3, 40, rs, is_, 7, None) == 108   # plane range
+    live = ctypes.c_int32()
+    assert L.lope_step_multi(h, ctypes.byref(lay), A, B, -1, rs, is_, None, ctypes.byref(live)) == 108
+    box = (ctypes.c_int64 * 3)(60, 0, 0)
+    ext = (ctypes.c_int64 * 3)(10, 1, 1)
+    assert L.lope_box_pack(ctypes.byref(lay), A, box, ext, B, None) == 108               # box leaves block
+    assert L.lope_copy_box(ctypes.byref(lay), A, B, box, box, ext, None) == 108
+    assert L.lope_plan_set(h, ctypes.byref(lay), 7, 99, 4, 0) == 108                     # no such variant
+    assert L.lope_ipc_close(ctypes.c_void_p(0x1234)) == 108                               # never opened
+    assert b"" != L.lope_last_error()
+    _lib.destroy_kernel(h)
