@@ -132,6 +132,37 @@ def periodic_apply_planes(get_planes, shape, kir, z0, z1, scalars=None, dtype=np
     return np.asarray(pending[kir.stored_arrays[0]], dtype=dtype)
 
 
+def periodic_apply_planes_steps(get_planes, shape, kir, z0, z1, steps, scalars=None, dtype=np.float64):
+    """Planes ``z0:z1`` (last axis) after ``steps`` applications of ``periodic_apply``.
+
+    Reads the window of planes the result depends on (``steps`` footprints beyond
+    each end, wrapped modulo the extent) and applies the kernel ``steps`` times, the
+    window shrinking by one footprint per step; the inner axes are whole and
+    periodic.  ``steps = 1`` is ``periodic_apply_planes``.  Sizes up to the full
+    BASELINE configurations stay a few planes of host memory.
+    """
+    fp = kir.footprints[kir.array_params[0]].dims
+    zn, zp = fp[-1]
+    n = shape[-1]
+    if steps <= 0:
+        return np.asarray(get_planes(np.arange(z0, z1) % n)).astype(dtype, copy=False)
+    slab = np.asarray(get_planes(np.arange(z0 - steps * zn, z1 + steps * zp) % n)).astype(dtype, copy=True)
+    inner = tuple(range(slab.ndim - 1))
+    for _ in range(steps):
+        nout = slab.shape[-1] - zn - zp
+        cur = slab
+
+        def read(name, offsets, cur=cur, nout=nout):
+            *oin, oz = offsets
+            s = cur[..., zn + oz: zn + oz + nout]
+            if any(o != 0 for o in oin):
+                s = np.roll(s, shift=tuple(-o for o in oin), axis=inner)
+            return s.copy()
+
+        slab = np.asarray(run_body(kir, read, scalars, dtype)[kir.stored_arrays[0]], dtype=dtype)
+    return slab
+
+
 def padded_shape(interior, lo, hi):
     return tuple(m + a + b for m, a, b in zip(interior, lo, hi))
 

@@ -644,6 +644,12 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     if (d.funcSetAttribute(m.tiledm, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tm_smem) != CUDA_SUCCESS ||
         d.occupancy(&nb, m.tiledm, m.tm_threads, m.tm_smem) != CUDA_SUCCESS || nb < 1)
       m.tiledm = nullptr;
+    // a register window that spills (wide footprints x 4 arrays) sends local memory
+    // through L2: such kernels run on the generic path instead
+    int lb = 0;
+    if (m.tiledm && d.funcGetAttribute(&lb, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, m.tiledm) == CUDA_SUCCESS &&
+        lb > 0 && !std::getenv("LOPE_MULTI_ALLOW_SPILL"))
+      m.tiledm = nullptr;
     m.tm_blocks = nb;
   } else {
     m.tiledm = nullptr;
@@ -1225,15 +1231,19 @@ int lope_launch(const lope_kernel* kc, const lope_layout* layouts, const int64_t
   }
   int r0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
   bool empty = false;
+  // runtime.py:583-595: every dim is bounds-checked (E108) before an empty range returns
+  for (int d = 0; d < ir.rank; ++d) {
+    int64_t lo = ranges[2 * d], hi = ranges[2 * d + 1];
+    if (lo < 1 || hi > layouts[0].interior[d])
+      return fail(108, "launch range %lld:%lld lies outside the interior 1:%lld in dim %d", (long long)lo,
+                  (long long)hi, (long long)layouts[0].interior[d], d + 1);
+  }
   for (int d = 0; d < ir.rank; ++d) {
     int64_t lo = ranges[2 * d], hi = ranges[2 * d + 1];
     if (lo > hi) {
       empty = true;
       continue;
     }
-    if (lo < 1 || hi > layouts[0].interior[d])
-      return fail(108, "launch range %lld:%lld lies outside the interior 1:%lld in dim %d", (long long)lo,
-                  (long long)hi, (long long)layouts[0].interior[d], d + 1);
     r0[d] = (int)(lo - 1);
     ext[d] = (int)(hi - lo + 1);
   }

@@ -878,15 +878,21 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
     const int gy0 = (s * FN1) / RY, gy1 = (HI - s * FP1 + RY - 1) / RY;
     const int ngx = gx1 - gx0, ntask = ngx * (gy1 - gy0);
     const int lane = threadIdx.x & 31;
-    for (int t = threadIdx.x; t < ntask; t += blockDim.x) {
+    // warp-uniform trip count (blockDim.x is a multiple of 32): every lane of a warp runs
+    // every iteration, so the full-mask shuffles below always see all 32 lanes; lanes
+    // past the last task compute a copy of it and store nothing
+    for (int t0 = threadIdx.x - lane; t0 < ntask; t0 += blockDim.x) {
+      const int tl = t0 + lane;
+      const bool act = tl < ntask;
+      const int t = act ? tl : ntask - 1;
       const int gxi = t % ngx;
       const int bx = (gx0 + gxi) * VX, by = (gy0 + t / ngx) * RY;
       const T* base = src + (by + PY) * WB + bx + PX;
-      // active lanes are a prefix of the warp (contiguous tasks); the x halo comes from
-      // the neighbouring lane unless that lane is another row, another warp or idle
-      const unsigned am = __activemask();
-      const bool own_l = lane == 0 || gxi == 0;
-      const bool own_r = lane == 31 || gxi == ngx - 1 || t + 1 >= ntask;
+      // the x halo comes from the neighbouring lane unless that lane holds another row,
+      // belongs to another warp or has no task of its own
+      constexpr unsigned am = 0xffffffffu;
+      const bool own_l = lane == 0 || gxi == 0 || !act;
+      const bool own_r = lane == 31 || gxi == ngx - 1 || tl + 1 >= ntask;
       T win[1][NR][NXW];
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
@@ -933,6 +939,7 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
           Body::template eval<T, false>(rd, sc.v, res, slow);
           vals[r][v] = res[0];
         }
+      if (!act) continue;
       if (s < TT) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {

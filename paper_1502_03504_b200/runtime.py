@@ -91,12 +91,22 @@ class HaloArray:
         """The live buffer (flat, ``layout.count`` elements)."""
         return self._bufs[self._live]
 
-    def spare(self):
-        """The other buffer of the ping-pong pair (allocated on first use)."""
+    def spare(self, stream=None):
+        """The other buffer of the ping-pong pair (allocated on first use).
+
+        The zero fill is enqueued on ``stream`` (default: the current stream), the
+        stream the caller is about to write the buffer on, so it can never land after
+        those writes."""
         torch = _torch()
         j = 1 - self._live
         if self._bufs[j] is None:
-            self._bufs[j] = torch.zeros_like(self._bufs[self._live])
+            if stream is None:
+                self._bufs[j] = torch.zeros_like(self._bufs[self._live])
+            else:
+                # the live buffer was filled on another stream: order against it first
+                stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(stream):
+                    self._bufs[j] = torch.zeros_like(self._bufs[self._live])
         return self._bufs[j]
 
     def swap(self) -> None:
@@ -457,7 +467,7 @@ def launch(kernel: CompiledKernel, arrays: Sequence[HaloArray], ranges=None,
     rng = (ctypes.c_int64 * (2 * rank))(*[int(v) for r in ranges for v in r])
     ins = (ctypes.c_void_p * na)(*[a.data.data_ptr() for a in arrays])
     stored = set(ir.stored_arrays)
-    outs = (ctypes.c_void_p * na)(*[(a.spare().data_ptr() if p in stored else None)
+    outs = (ctypes.c_void_p * na)(*[(a.spare(stream).data_ptr() if p in stored else None)
                                     for p, a in zip(ir.array_params, arrays)])
     rs, is_ = kernel.scalar_args(scalars)
     _lib.check(_lib.lib().lope_launch(kernel.handle, layouts, rng, ins, outs, rs, is_,
@@ -496,7 +506,7 @@ def _step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Optio
     rs, is_ = kernel.scalar_args(scalars)
     _lib.check(_lib.lib().lope_step(kernel.handle, ctypes.byref(arr.layout),
                                     ctypes.c_void_p(arr.data.data_ptr()),
-                                    ctypes.c_void_p(arr.spare().data_ptr()), rs, is_, mask,
+                                    ctypes.c_void_p(arr.spare(stream).data_ptr()), rs, is_, mask,
                                     ctypes.c_void_p(_stream_handle(stream))), "lope_step")
     arr.swap()
     if tuner is not None:
@@ -517,7 +527,7 @@ def _multi_step(kernel: CompiledKernel, arr: HaloArray, nsteps: int, scalars=Non
         return
     rs, is_ = kernel.scalar_args(scalars)
     live = ctypes.c_int32()
-    a, b = arr.data, arr.spare()
+    a, b = arr.data, arr.spare(stream)
     _lib.check(_lib.lib().lope_step_multi(kernel.handle, ctypes.byref(arr.layout), ctypes.c_void_p(a.data_ptr()),
                                           ctypes.c_void_p(b.data_ptr()), int(nsteps), rs, is_,
                                           ctypes.c_void_p(_stream_handle(stream)), ctypes.byref(live)),
@@ -562,7 +572,17 @@ def run_pinned(kernel: CompiledKernel, shape, lo, hi, dtype, host_in, host_out, 
     column-major order (numpy ``order='F'``).  Returns after the download
     has completed.
     """
-    arr = HaloArray(shape, lo, hi, dtype)
+    torch = _torch()
+    if stream is None:
+        arr = HaloArray(shape, lo, hi, dtype)
+        arr.spare()
+    else:
+        # both ping-pong buffers are zero-filled on `stream` itself, before the upload
+        # and the steps enqueued there (a fill left on another stream could land later)
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            arr = HaloArray(shape, lo, hi, dtype)
+            arr.spare()
     arr.upload(host_in.data_ptr(), stream)
     iterate(kernel, arr, steps, scalars, stream)
     arr.download(host_out.data_ptr(), stream)
@@ -571,6 +591,9 @@ def run_pinned(kernel: CompiledKernel, shape, lo, hi, dtype, host_in, host_out, 
 
 class StepGraph:
     """``steps`` fused steps captured once as a CUDA graph and replayed.
+
+    Construction does not advance the field (the warm-up runs on a scratch block);
+    each ``replay()`` advances it by ``steps`` fused steps.
 
     For small (L2-resident) fields the per-launch host cost dominates (config 1:
     1024^2 in ~3 us of GPU time); a graph replays the whole chain with one
@@ -588,12 +611,19 @@ class StepGraph:
         arr.spare()                       # both ping-pong buffers exist before capture
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):        # warm the module / tensor-map caches off-graph
+        with torch.cuda.stream(s):
+            # warm the module / launch caches off-graph on a scratch block of the same
+            # geometry: the caller's field is not advanced by the warm-up
+            scratch = HaloArray(arr.interior, arr.lo, arr.hi,
+                                "float32" if arr.dtype_code == _lib.F32 else "float64", device=arr.device)
+            scratch.spare(s)
             if multi:
-                multi_step(kernel, arr, 4, scalars, stream=s)
-            step(kernel, arr, scalars, stream=s)
-            step(kernel, arr, scalars, stream=s)
+                multi_step(kernel, scratch, 4, scalars, stream=s)
+            step(kernel, scratch, scalars, stream=s)
+            step(kernel, scratch, scalars, stream=s)
         torch.cuda.current_stream().wait_stream(s)
+        s.synchronize()
+        del scratch
         self.graph = torch.cuda.CUDAGraph()
         l0 = _lib.launch_count()
         with torch.cuda.graph(self.graph):

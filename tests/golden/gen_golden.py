@@ -17,7 +17,10 @@ reference ``Machine`` / ``oracle_step`` in float64 and writes small fixtures:
   ``HALO_TRANSFER`` on slab-decomposed grids (``runtime.py:643-711``);
 * ``random.npz`` + ``random.json`` — random kernels (offsets in [-2,2], + - * /,
   abs/min/max/sqrt, scalar parameters, locals) with one ``oracle_step``;
-* ``kats.json``     — point-source / corner / fixed-point / layout KATs.
+* ``kats.json``     — point-source / corner / fixed-point / layout KATs;
+* ``config_digests.json`` (``--configs``) — SHA-256 of the reference ``Machine``'s
+  fp64 output at the exact BASELINE sizes it can run (configs 1, 2 and 4, the last
+  one slab-decomposed over 8 images).
 
 Nothing here runs on the GPU box; the fixtures travel, the reference does not.
 """
@@ -476,8 +479,69 @@ def gen_machine():
     (HERE / "machine.json").write_text(json.dumps(cases, indent=1) + "\n")
 
 
+def column_major_digest(a):
+    """SHA-256 of an array's values in column-major (reference block) order."""
+    import hashlib
+    f = np.asfortranarray(a)
+    return hashlib.sha256(memoryview(f.T)).hexdigest()
+
+
+def hash_field_chunked(shape, seed, chunk=1024):
+    """oracle.hash_field(shape, seed, float64) built a few planes at a time (bounded memory)."""
+    from oracle.lope_oracle import hash_planes
+    out = np.empty(shape, dtype=np.float64, order="F")
+    n = shape[-1]
+    for z0 in range(0, n, chunk):
+        z1 = min(n, z0 + chunk)
+        out[..., z0:z1] = hash_planes(shape, seed, np.arange(z0, z1), np.float64)
+    return out
+
+
+# BASELINE configurations the reference Machine itself can run (rank 2; fp64, its only
+# precision), at their exact sizes; the input is the device hash field (seed 20260823).
+CONFIG_RUNS = (
+    # tag, kernel, shape, steps, images, grid_rows
+    ("c1", "heat2d", (1024, 1024), 100, 1, 1),
+    ("c1_p4", "heat2d", (1024, 1024), 100, 4, 4),
+    ("c2", "ninept2d", (16384, 16384), 1, 1, 1),
+    ("c4_p8", "box5x5", (32768, 32768), 1, 8, 8),
+)
+
+
+def gen_config_digests(only=None):
+    """SHA-256 digests of the reference Machine's output at the BASELINE config sizes
+    (runtime.py:308-337 via Machine.run / gather), for the full-size GPU parity tests.
+    Too large to commit as arrays; the digest and a few sampled values travel."""
+    import time
+    path = HERE / "config_digests.json"
+    out = json.loads(path.read_text()) if path.exists() else {}
+    for tag, kname, shape, steps, images, rows in CONFIG_RUNS:
+        if only and tag not in only:
+            continue
+        t0 = time.time()
+        field = hash_field_chunked(shape, 20260823)
+        result = program_for(kname)
+        m = run_machine(result, field, images=images, grid_rows=rows, steps=steps)
+        del field
+        got = m.gather()
+        del m
+        samples = [[int(i), int(j), float(got[i, j])]
+                   for i, j in ((0, 0), (shape[0] - 1, shape[1] - 1), (shape[0] // 2, shape[1] // 3),
+                                (1, shape[1] - 2))]
+        out[tag] = {"kernel": kname, "shape": list(shape), "dtype": "float64", "steps": steps,
+                    "seed": 20260823, "images": images, "grid_rows": rows,
+                    "sha256_column_major": column_major_digest(got), "samples": samples,
+                    "seconds": round(time.time() - t0, 1)}
+        del got
+        print(tag, out[tag]["sha256_column_major"], out[tag]["seconds"], "s", flush=True)
+        path.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
+
+
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    if "--configs" in sys.argv:
+        gen_config_digests([a for a in sys.argv[2:]] or None)
+        sys.exit(0)
     gen_kernels()
     gen_runs()
     gen_exchange()

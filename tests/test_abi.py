@@ -188,5 +188,10 @@ def test_boundary_rejects_bad_calls_with_reference_codes():
     assert L.lope_copy_box(ctypes.byref(lay), A, B, box, box, ext, None) == 108
     assert L.lope_plan_set(h, ctypes.byref(lay), 7, 99, 4, 0) == 108                     # no such variant
     assert L.lope_ipc_close(ctypes.c_void_p(0x1234)) == 108                               # never opened
+    # lope_launch bounds-checks every dim before an empty range returns (runtime.py:583-595)
+    ins = (ctypes.c_void_p * 1)(A)
+    outs = (ctypes.c_void_p * 1)(B)
+    for rng in ((0, -1, 1, 32, 1, 16), (1, 64, 1, 32, 20, 17), (1, 64, 5, 3, 1, 17)):
+        assert L.lope_launch(h, ctypes.byref(lay), (ctypes.c_int64 * 6)(*rng), ins, outs, rs, is_, None) == 108, rng
     assert b"" != L.lope_last_error()
     _lib.destroy_kernel(h)

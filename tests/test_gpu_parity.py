@@ -207,6 +207,10 @@ def test_empty_range_and_faults():
     with pytest.raises(RuntimeFault) as e:
         R.launch(k, [arr], [(1, 9), (1, 8)])
     assert e.value.code == "E108"
+    for rng in ([(0, -1), (1, 8)], [(1, 8), (3, 9)], [(20, 10), (1, 8)]):   # empty but out of bounds
+        with pytest.raises(RuntimeFault) as e:
+            R.launch(k, [arr], rng)
+        assert e.value.code == "E108", rng
     thin = R.HaloArray((8, 8), (0, 1), (1, 1), "float64")
     with pytest.raises(RuntimeFault) as e:
         R.launch(k, [thin])
@@ -343,12 +347,13 @@ def test_step_graph_with_temporal_blocking_matches_single_steps():
     a = R.HaloArray(field.shape, [1, 1], [1, 1], "float32")
     a.set_interior(field)
     R.halo_transfer(a)
-    g = R.StepGraph(k, a, 16)          # warm-up inside advances the field by 6 steps
+    g = R.StepGraph(k, a, 16)          # construction leaves the field alone
+    assert O.equal_bits(a.get_interior(), field)
     g.replay()
     torch.cuda.synchronize()
     assert g.launches < 16
     want = field
-    for _ in range(22):
+    for _ in range(16):
         want = O.periodic_apply(want, kir, None, np.float32)
     assert O.equal_bits(a.get_interior(), want)
 
@@ -475,3 +480,23 @@ def test_multi_array_tiled_equals_generic(monkeypatch, rank, na, dt):
         monkeypatch.delenv("LOPE_FORCE_GENERIC", raising=False)
     for a_, b_ in zip(*outs):
         assert O.equal_bits(a_, b_)
+
+
+def test_run_pinned_on_a_side_stream_with_the_default_stream_busy():
+    """buffers used on a caller's stream are zero-filled on that stream, so a
+    busy default stream cannot delay a fill past the upload or the first step's stores."""
+    kir = stencils.heat2d()
+    shape = (512, 384)
+    field = O.hash_field(shape, 41, np.float32)
+    host_in = torch.from_numpy(np.asfortranarray(field).ravel(order="K").copy()).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    side = torch.cuda.Stream()
+    k = K(kir, "float32")
+    torch.cuda._sleep(200_000_000)               # ~0.1 s of work queued on the default stream
+    R.run_pinned(k, shape, (1, 1), (1, 1), "float32", host_in, host_out, 9, stream=side)
+    got = host_out.numpy().reshape(shape, order="F")
+    want = field
+    for _ in range(9):
+        want = O.periodic_apply(want, kir, None, np.float32)
+    assert O.equal_bits(got, want)
+    torch.cuda.synchronize()

@@ -133,3 +133,17 @@ def test_hash_field_is_decomposition_independent():
     assert O.equal_bits(planes, full[..., 3:7])
     v = O.hash_field((1000,), 1)
     assert v.min() >= -1.0 and v.max() < 1.0 and abs(v.mean()) < 0.1
+
+
+def test_periodic_apply_planes_steps_equals_dense_steps():
+    """The windowed multi-step restatement (full-size sampled checks) equals K dense steps."""
+    for name, shape in (("lap3d7", (12, 10, 16)), ("box5x5", (20, 24)), ("heat2d", (9, 30))):
+        kir = stencils.by_name(name)
+        f = O.hash_field(shape, 3, np.float64)
+        want = f
+        for s in range(1, 5):
+            want = O.periodic_apply(want, kir, None, np.float64)
+            for z0, z1 in ((0, 2), (5, 7), (shape[-1] - 2, shape[-1])):
+                got = O.periodic_apply_planes_steps(lambda idx: O.hash_planes(shape, 3, idx, np.float64),
+                                                    shape, kir, z0, z1, s, None, np.float64)
+                assert O.equal_bits(got, want[..., z0:z1]), (name, s, z0)
