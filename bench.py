@@ -12,7 +12,7 @@ Workloads (BASELINE.json configs; default c3, the HBM-roofline headline):
   c1  heat2d   1024^2      fp32  (L2-resident, launch-bound)
   c2  ninept2d 16384^2     fp32
   c3  lap3d7   1024^3      fp32  per GPU (N>1: slab-decomposed along z, weak scaling)
-  c4  box5x5   32768^2     fp64  (N>1: 32768 x 32768*N, slabs along y, weak scaling)
+  c4  box5x5   32768^2     fp64  (N>1: the same domain in N slabs along y, strong scaling)
   c5  lap3d7   2048^3      fp32  per GPU
 
 ``value`` = interior points x steps (all ranks) / max-over-ranks device time,
@@ -48,8 +48,9 @@ WORKLOADS = {
                desc="2D 9-point 16384x16384 fp32, halo 1 (config 2)"),
     "c3": dict(kernel="lap3d7", shape=(1024, 1024, 1024), dtype="float32", split=2,
                desc="3D 7-point 1024^3 fp32 per GPU, halo 1 (config 3; N>1 weak-scaled slabs along z)"),
-    "c4": dict(kernel="box5x5", shape=(32768, 32768), dtype="float64", split=1,
-               desc="2D 5x5 box 32768x32768 fp64 per GPU, halo 2 (config 4; N>1 slabs along y)"),
+    "c4": dict(kernel="box5x5", shape=(32768, 32768), dtype="float64", split=1, scaling="strong",
+               desc="2D 5x5 box 32768x32768 fp64, halo 2 (config 4; N>1: the fixed domain split into "
+                    "N slabs along y, 32768 x 32768/N per GPU, strong scaling)"),
     "c5": dict(kernel="lap3d7", shape=(2048, 2048, 2048), dtype="float32", split=2,
                desc="3D 7-point 2048^3 fp32 per GPU, halo 1 (config 5, weak scaling)"),
 }
@@ -83,17 +84,34 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+def plan_signature(plan):
+    """(tile, producer_warp, shfl, nb, zchunk) of a plan as lope_kernel_describe lists it."""
+    if not plan:
+        return None
+    return (tuple(plan.get("tile", ())), plan.get("producer_warp"), plan.get("shfl"), plan.get("nb"),
+            plan.get("zchunk"))
+
+
+def ncu_traffic(workload, plan):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from a committed ncu
+    capture of the SAME workload under the SAME execution plan (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py); None when no capture of this plan exists."""
     p = REPO / "profiles" / "ncu_traffic.json"
-    if p.exists():
-        try:
-            d = json.loads(p.read_text())
-            if workload in d:
-                return d[workload]
-        except Exception:
-            pass
-    return None
+    if not p.exists():
+        return None, "no ncu capture committed"
+    try:
+        d = json.loads(p.read_text())
+    except ValueError:
+        return None, "unreadable profiles/ncu_traffic.json"
+    sig = plan_signature(plan)
+    others = []
+    for e in d.get("entries", []):
+        if e.get("workload") != workload:
+            continue
+        if sig is not None and plan_signature(e.get("plan")) == sig:
+            return int(e["dram_read_bytes"] + e["dram_write_bytes"]), e.get("source")
+        others.append(e.get("plan"))
+    return None, f"no capture of this plan (captured plans: {others})"
 
 
 class ClockSampler:
@@ -163,13 +181,60 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (the numpy port of the reference's vectorised launch)
+# CPU reference: the reference's own Machine (baseline/_ref lopec) where it can run
+# the workload within the time budget, else the threaded numpy port of its
+# vectorised launch (oracle/) at full size, else a slab sample of it.
+
+REF_BUDGET_S = float(os.environ.get("LOPE_BENCH_REF_BUDGET_S", "240"))
+# single-thread fp64 Machine throughput measured in the survey, used
+# only to decide whether K Machine steps fit the budget
+MACHINE_GPTS_EST = 0.03
 
 
-def cpu_reference(wl, seconds=10.0, max_steps=None):
-    """Time the reference algorithm (halo transfer + run_body launch, fp as the workload)
-    on a bounded sample: the first planes of the workload's field along the
-    slowest axis, all host threads."""
+def host_ram_bytes():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 0
+
+
+def _lopec():
+    """The unmodified reference package, installed under baseline/_ref."""
+    ref = REPO / "baseline" / "_ref"
+    if (ref / "lopec" / "__init__.py").exists() and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import lopec
+    return lopec
+
+
+def _hash_block(shape, lo, hi, npdt, pool=None, planes_per_task=8):
+    """Padded column-major block (the reference's layout, ir.py:189-230) holding the
+    device hash field (oracle.hash_planes == lope_fill_hash), zero halo."""
+    import numpy as np
+
+    from oracle import lope_oracle as O
+    pshape = tuple(m + a + b for m, a, b in zip(shape, lo, hi))
+    blk = np.zeros(pshape, dtype=npdt, order="F")
+    n = shape[-1]
+    inner = tuple(slice(a, a + m) for a, m in zip(lo[:-1], shape[:-1]))
+
+    def fill(z0):
+        z1 = min(n, z0 + planes_per_task)
+        blk[inner + (slice(lo[-1] + z0, lo[-1] + z1),)] = O.hash_planes(shape, SEED, np.arange(z0, z1), npdt)
+
+    tasks = range(0, n, planes_per_task)
+    if pool is not None:
+        list(pool.map(fill, tasks))
+    else:
+        for z in tasks:
+            fill(z)
+    return blk
+
+
+def cpu_port(wl, steps, warm, budget_s, shape=None):
+    """The threaded numpy port of Machine._halo_exchange + _launch_vector (oracle/),
+    all host threads, in the workload's dtype.  Full size when the time budget and
+    host memory allow, otherwise a slab of the slowest axis (stated in `sample`)."""
     import numpy as np
     from concurrent.futures import ThreadPoolExecutor
 
@@ -178,55 +243,116 @@ def cpu_reference(wl, seconds=10.0, max_steps=None):
 
     kir = stencils.by_name(wl["kernel"])
     npdt = np.float32 if wl["dtype"] == "float32" else np.float64
-    shape = list(wl["shape"])
-    # bounded sample: keep the leading dims, cut the slowest one to ~32M points
-    inner = int(np.prod(shape[:-1]))
-    shape[-1] = max(4, min(shape[-1], (1 << 25) // inner))
-    if len(shape) == 2 and inner > (1 << 24):
-        shape = [1 << 14, 1 << 11]
+    shape = list(shape or wl["shape"])
+    full = list(shape)
     fp = kir.footprints[kir.array_params[0]].dims
     lo, hi = [n for n, _ in fp], [p for _, p in fp]
-    f = O.hash_field(tuple(shape[::-1]), SEED, npdt).T     # C-ordered block, reference index order
-    blk = O.embed(np.ascontiguousarray(f), lo, hi, npdt)
+    esz = np.dtype(npdt).itemsize
+    pts = int(np.prod(shape))
     threads = os.cpu_count() or 1
     pool = ThreadPoolExecutor(threads)
-    O.threaded_machine_step(blk, lo, hi, kir, None, npdt, pool, threads)     # warm-up
+    # calibrate on a slab of ~16M points, then fit the budget and half the host memory
+    # (block + snapshot)
+    inner = pts // shape[-1]
+    probe = list(shape)
+    probe[-1] = max(4, min(shape[-1], (1 << 24) // max(1, inner)))
+    pblk = _hash_block(probe, lo, hi, npdt, pool)
     t0 = time.perf_counter()
-    n = 0
-    while True:
+    O.threaded_machine_step(pblk, lo, hi, kir, None, npdt, pool, threads)
+    rate = int(np.prod(probe)) / max(1e-9, time.perf_counter() - t0)
+    del pblk
+    frac = min(1.0, budget_s / max(1e-9, (steps + warm) * pts / rate))
+    ram = host_ram_bytes()
+    if ram:
+        frac = min(frac, 0.5 * ram / (2.2 * pts * esz))
+    if frac < 1.0:
+        shape[-1] = max(4, int(shape[-1] * frac))
+    t_gen = time.perf_counter()
+    blk = _hash_block(shape, lo, hi, npdt, pool)
+    t_gen = time.perf_counter() - t_gen
+    for _ in range(warm):
         O.threaded_machine_step(blk, lo, hi, kir, None, npdt, pool, threads)
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or (max_steps and n >= max_steps):
-            break
+    per = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.threaded_machine_step(blk, lo, hi, kir, None, npdt, pool, threads)
+        per.append(time.perf_counter() - t0)
+    pool.shutdown()
+    el = sum(per)
     pts = int(np.prod(shape))
-    return {"value": pts * n / el / 1e9, "unit": "Gpoints/s", "cores": threads, "kind": "port",
-            "sample": f"{n} step(s) of {kir.name} on {'x'.join(map(str, shape))} {wl['dtype']} "
-                      f"(numpy port of lopec Machine._halo_exchange + _launch_vector, "
-                      f"{threads} threads), {el:.1f} s"}
+    same = shape == full
+    return {"value": pts * steps / el / 1e9 if el > 0 else None, "unit": "Gpoints/s", "cores": threads,
+            "kind": "port", "same_config": same, "steps": steps, "seconds": round(el, 3),
+            "ms_per_step": round(1e3 * el / max(1, steps), 3),
+            "sample": (f"{steps} step(s) of {kir.name} on {'x'.join(map(str, shape))} {wl['dtype']}"
+                       f"{' (the full workload)' if same else ' (slab of the full ' + 'x'.join(map(str, full)) + ')'}"
+                       f": numpy port of lopec Machine._halo_exchange + _launch_vector (oracle/lope_oracle.py "
+                       f"threaded_machine_step), {threads} host threads, {el:.1f} s timed, input generation "
+                       f"{t_gen:.1f} s untimed")}
+
+
+def reference_machine(wl, steps, warm):
+    """The reference's own ``Machine`` (baseline/_ref, unmodified) running the config's
+    program -- HALO_TRANSFER + device launch per iteration (runtime.py:308-337) -- in
+    fp64, its only precision, on one host thread (numpy ufuncs are single-threaded)."""
+    import numpy as np
+
+    from oracle.lope_programs import program_text
+    lopec = _lopec()
+    from lopec.runtime import Machine, RunConfig
+    prog, diags = lopec.parse_source(program_text(wl["kernel"]), f"{wl['kernel']}.lope")
+    if prog is None or diags:
+        raise RuntimeError(f"reference frontend rejected the program: {diags}")
+    chk = lopec.check_program(prog)
+    shape = tuple(wl["shape"])
+    field = np.asfortranarray(_hash_block(shape, [0] * len(shape), [0] * len(shape), np.float64))
+    if warm:
+        Machine(chk, RunConfig(images=1, steps=warm), field.copy()).run()
+    m = Machine(chk, RunConfig(images=1, steps=steps), field)
+    t0 = time.perf_counter()
+    m.run()
+    el = time.perf_counter() - t0
+    pts = int(np.prod(shape))
+    return {"value": pts * steps / el / 1e9, "unit": "Gpoints/s", "cores": 1, "kind": "reference",
+            "same_config": True, "steps": steps, "seconds": round(el, 3),
+            "ms_per_step": round(1e3 * el / max(1, steps), 3), "precision": "f64",
+            "sample": (f"lopec.Machine(check, RunConfig(images=1, steps={steps})).run() from baseline/_ref "
+                       f"(unmodified reference) on {wl['kernel']} {'x'.join(map(str, shape))}, fp64 (the "
+                       f"reference's only precision), 1 numpy thread of {os.cpu_count()} host cores, "
+                       f"{el:.2f} s")}
+
+
+def cpu_reference_full(wl, steps, warm, budget_s=REF_BUDGET_S):
+    """The reference arm's measurement: the reference Machine when the config is rank <= 2
+    and K + W of its steps fit the budget, else the port (full size when it fits)."""
+    import numpy as np
+    pts = int(np.prod(wl["shape"]))
+    if len(wl["shape"]) <= 2 and (steps + warm) * pts / (MACHINE_GPTS_EST * 1e9) <= budget_s:
+        try:
+            return reference_machine(wl, steps, warm)
+        except Exception as e:             # pragma: no cover - reference install missing
+            log("reference Machine unavailable, timing the port:", e)
+    return cpu_port(wl, steps, warm, budget_s)
 
 
 def run_reference_arm(args, wl):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
     steps, warm = args.steps, args.warmup
-    # each step: a bounded CPU sample; scale to a few minutes in total
-    per = max(0.5, min(5.0, 120.0 / max(1, steps + warm)))
-    cpu_reference(wl, seconds=per * warm if warm else 0.1, max_steps=max(1, warm))
-    res = cpu_reference(wl, seconds=per * steps, max_steps=steps)
+    res = cpu_reference_full(wl, steps, warm)
     line = {
         "metric": "stencil Gpoints/s & HBM GB/s (% of 8 TB/s roofline) at 1/2/4/8 B200 vs CPU ref",
         "impl": "reference", "value": res["value"], "unit": "Gpoints/s", "n_gpus": ws,
         "steps": steps, "warmup": warm,
-        # the sample's rate extrapolated to one step over the whole workload
-        "ms_per_step": round(float(np.prod(wl["shape"])) / res["value"] / 1e6, 3) if res.get("value") else None,
+        # measured per step of what ran (the full workload unless `same_config` is false)
+        "ms_per_step": res["ms_per_step"],
         "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl["dtype"] == "float32" else "f64",
-        "data": "synthetic (splitmix64 U(-1,1) field)",
+        "scaling": wl.get("scaling", "weak"), "vs_baseline": None,
+        "dtype": "f64" if res.get("precision") == "f64" or wl["dtype"] == "float64" else "f32",
+        "data": "synthetic (splitmix64 U(-1,1) hash field, the GPU arm's input)",
         "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
-                   "shape_per_gpu": list(wl["shape"])},
+                   "shape_per_gpu": list(wl["shape"]), "same_config": bool(res.get("same_config"))},
         "cpu_baseline": res,
         "e2e": {"value": res["value"], "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -266,7 +392,11 @@ def run_gpu_arm(args, wl):
     exchange_kind = None
     fp = kir.footprints[kir.array_params[0]].dims
     lo, hi = [n for n, _ in fp], [p for _, p in fp]
-    shape = tuple(wl["shape"])
+    strong = wl.get("scaling", "weak") == "strong"
+    gshape = tuple(wl["shape"]) if strong else tuple(wl["shape"][:-1]) + (wl["shape"][-1] * ws,)
+    if gshape[-1] % ws:
+        raise SystemExit(f"{args.workload}: {gshape[-1]} planes do not split over {ws} GPUs")
+    shape = tuple(gshape[:-1]) + (gshape[-1] // ws,)      # this rank's slab
     esz = 4 if wl["dtype"] == "float32" else 8
     points = int(np.prod(shape))
     stream = torch.cuda.current_stream()
@@ -274,9 +404,8 @@ def run_gpu_arm(args, wl):
     if ws > 1:
         from paper_1502_03504_b200 import dist as D
         field = D.SlabArray(shape, lo, hi, wl["dtype"], group=group)
-        gext = list(shape[:-1]) + [shape[-1] * ws]
         gorg = [0] * (len(shape) - 1) + [shape[-1] * rank]
-        field.block.fill_hash(SEED, gext, gorg)
+        field.block.fill_hash(SEED, list(gshape), gorg)
         # fused exchange: the kernel stores boundary planes into the neighbours' halos
         # through CUDA IPC peer memory; NCCL send/recv overlapped with the interior if
         # the peer mapping is unavailable
@@ -302,6 +431,15 @@ def run_gpu_arm(args, wl):
         def do_step():
             R.step(kern, arr)
 
+    if args.plan:
+        # replay a recorded plan instead of tuning (profiling captures of one plan)
+        import ctypes
+        os.environ["LOPE_AUTOTUNE"] = "0"
+        cfg, zc = args.plan.split(":")
+        vals = [int(v) for v in cfg.split(",")]
+        _lib.check(_lib.lib().lope_plan_set_variant(kern.handle, ctypes.byref(arr.layout), (1 << arr.rank) - 1,
+                                                    (ctypes.c_int32 * 8)(*vals), int(zc), 0, None),
+                   "lope_plan_set_variant")
     # plan selection (runtime.PlanTuner): real steps under each candidate plan, part
     # of setup like compilation; the timed steps run the chosen plan
     tune_steps = 0
@@ -388,22 +526,60 @@ def run_gpu_arm(args, wl):
     alg_bytes = 2 * esz * points
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    chosen = json.loads(kern.describe()).get("plans") or {}
+    plan = next(iter(chosen.values()), None)
+    if graph is not None:
+        plan = {"kernel": "lope_tblock"}
+    traffic, traffic_src = ncu_traffic(args.workload, plan)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload),
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
                 "kernel_ms": round(kernel_ms, 4),
                 "step_ms_min_med_max": [round(min(per_step), 4), round(sorted(per_step)[len(per_step) // 2], 4),
                                         round(max(per_step), 4)],
                 "pct_of_8TBs": round(100 * alg_bytes / (kernel_ms / 1e3) / 8e12, 1)}
 
+    # sustained: the same step for >= `--sustained-seconds` of device time right after
+    # the timed window (the board's power cap engages within ~0.5 s on every large
+    # config; this is the rate a long run settles at)
+    sustained = None
+    if args.sustained_seconds > 0:
+        per_launch = ms_per_step * (steps_done if graph is not None else 1)
+        nrep = int(min(50000, max(3, math.ceil(1e3 * args.sustained_seconds / max(per_launch, 1e-4)))))
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nrep)]
+        barrier()
+        with ClockSampler(local) as sclk:
+            for i in range(nrep):
+                sev[i][0].record(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    do_step()
+                sev[i][1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        d = sorted(a.elapsed_time(b) / (steps_done if graph is not None else 1) for a, b in sev)
+        med = d[len(d) // 2]
+        tot = sum(d) * (steps_done if graph is not None else 1) / 1e3
+        sustained = {"steps": nrep * (steps_done if graph is not None else 1), "seconds": round(tot, 3),
+                     "ms_per_step_median": round(med, 4),
+                     "value_median": round(points * ws / (med / 1e3) / 1e9, 3),
+                     "pct_of_8TBs_median": round(100 * 2 * esz * points / (med / 1e3) / 8e12, 1),
+                     "frac_of_measured_peak_median": round(2 * esz * points / (med / 1e3) / 1e9 / measured_peak()[0], 4),
+                     "clocks": sclk.summary(),
+                     "note": "per-rank device time of rank 0" if ws > 1 else "device time, CUDA events per step"}
+
     # e2e through the public API, host buffers, H2D + E2E_ITERS iterations + D2H timed
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev)
+        e2e = e2e_measure(args, wl, kern, lo, hi, shape, gshape, esz, group, ws, rank, dev)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_reference(wl, seconds=args.cpu_seconds)
+        # bounded: a couple of full-size steps (config 1: the reference Machine itself)
+        small = int(np.prod(wl["shape"])) <= (1 << 22)
+        cpu = cpu_reference_full(wl, steps=args.steps if small else 2, warm=1 if small else 0,
+                                 budget_s=args.cpu_seconds)
 
     del arr
     if rank == 0:
@@ -412,11 +588,11 @@ def run_gpu_arm(args, wl):
             "value": round(value, 3), "unit": "Gpoints/s", "n_gpus": ws, "steps": args.steps,
             "cuda_graph": graph is not None,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": wl.get("scaling", "weak"), "vs_baseline": None,
             "dtype": "f32" if wl["dtype"] == "float32" else "f64",
             "data": "synthetic (splitmix64 U(-1,1) field generated on device)",
             "config": {"workload": args.workload, "desc": wl["desc"], "kernel": wl["kernel"],
-                       "shape_per_gpu": list(shape), "global_shape": list(shape[:-1]) + [shape[-1] * ws],
+                       "shape_per_gpu": list(shape), "global_shape": list(gshape),
                        "halo": [lo, hi], "parallelism": f"slab{ws}" if ws > 1 else "single",
                        "exchange": exchange_kind if ws > 1 else "in-kernel periodic images",
                        "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
@@ -426,6 +602,7 @@ def run_gpu_arm(args, wl):
                      "extra_warmup_steps": extra,
                      "watchdog_fallback": [t.report.get("fallback") for t in kern._tuners.values()]},
             "roofline": roofline,
+            "sustained": sustained,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -437,8 +614,12 @@ def run_gpu_arm(args, wl):
         dist.destroy_process_group()
 
 
-def e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev):
-    """Public API, host (pinned) buffers: upload, E2E_ITERS iterations, download."""
+def e2e_measure(args, wl, kern, lo, hi, shape, gshape, esz, group, ws, rank, dev):
+    """Public API, host (pinned) buffers: upload, E2E_ITERS iterations, download.
+
+    The input is this rank's slab of the hash field (the device-timed run's input, so
+    data-dependent paths such as flagged divisions see the same values), produced on
+    the device and downloaded into the pinned buffer before the timed region."""
     import numpy as np
     import torch
 
@@ -447,7 +628,12 @@ def e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev):
     nbytes = int(np.prod(shape)) * esz
     tdt = torch.float32 if esz == 4 else torch.float64
     host_in = torch.empty(nbytes // esz, dtype=tdt, pin_memory=True)
-    host_in.numpy()[:] = 0.5
+    src = R.HaloArray(shape, lo, hi, wl["dtype"])
+    src.fill_hash(SEED, list(gshape), [0] * (len(shape) - 1) + [shape[-1] * rank])
+    src.download(host_in.data_ptr())
+    torch.cuda.synchronize()
+    del src
+    torch.cuda.empty_cache()
     host_out = torch.empty_like(host_in, pin_memory=True)
     if ws > 1:
         from paper_1502_03504_b200 import dist as D
@@ -477,7 +663,8 @@ def e2e_measure(args, wl, kern, lo, hi, shape, esz, group, ws, rank, dev):
     return {"value": round(pts / el / 1e9, 3), "unit": "Gpoints/s",
             "h2d_bytes_per_step": nbytes // E2E_ITERS, "d2h_bytes_per_step": nbytes // E2E_ITERS,
             "iters_per_call": E2E_ITERS, "calls": reps, "seconds": round(el, 4),
-            "api": "runtime.run_pinned (HaloArray upload, iterate, gather)"}
+            "api": "runtime.run_pinned (HaloArray upload, iterate, gather)",
+            "input": "hash field slab in pinned host memory (column-major)"}
 
 
 def main():
@@ -489,7 +676,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--sustained-seconds", type=float, default=1.0)
+    ap.add_argument("--plan", default=None,
+                    help="replay a plan 'bxw,wy,ry,ns,pw,mb,sh,nb:zchunk' instead of tuning (ncu captures)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")

@@ -177,6 +177,11 @@ int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, 
  * ctas_per_sm} (compiled if needed); *variant (may be NULL) receives its index. */
 int lope_plan_set_tile(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, const int32_t* tile,
                        int32_t zchunk, int32_t yband, int32_t* variant);
+/* Every plan parameter: cfg = {bxw, wy, ry, ns, producer_warp, ctas_per_sm, shfl, nb}
+ * (the "tile", "producer_warp", "shfl", "nb" fields of lope_kernel_describe's plans);
+ * replays a plan recorded by an earlier run (profiling captures of a given plan). */
+int lope_plan_set_variant(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, const int32_t* cfg,
+                          int32_t zchunk, int32_t yband, int32_t* variant);
 
 /* Box <-> contiguous device buffer (column-major within the box, dim 1 fastest):
  * `extent` cells at padded coordinates `lo`.  Faces of a decomposed dimension other

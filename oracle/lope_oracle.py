@@ -372,27 +372,56 @@ def gpts(points, seconds):
 def threaded_machine_step(blk, lo, hi, kir, scalars=None, dtype=np.float64, pool=None, nthreads=1):
     """One ``HALO_TRANSFER`` + full-interior launch on padded block ``blk`` (in place).
 
-    The launch range is split along the block's slowest-varying memory axis
-    (axis 0 for the C-ordered blocks used here) so each thread streams its own
-    contiguous chunk; the arithmetic is ``run_body``'s, unchanged.
+    The launch range is cut into tiles of about 128K points along the block's two
+    slowest-varying memory axes, so every thread's numpy temporaries stay in its
+    cache; each tile is one ``_launch_vector`` over its sub-range (the arithmetic is
+    ``run_body``'s, unchanged, and tiles write disjoint cells of the live buffer
+    while reading the snapshot).  The snapshot copy (runtime.py:596) is split the
+    same way across the threads.
     """
     halo_fill(blk, lo, hi)
-    snap = blk.copy()                                   # runtime.py:596 snapshot
     shape = tuple(s - a - b for s, a, b in zip(blk.shape, lo, hi))
-    ax = 0 if blk.flags.c_contiguous else blk.ndim - 1
-    n = shape[ax]
-    plane = max(1, int(np.prod(shape)) // n)
-    chunk = max(1, (1 << 17) // plane)              # ~128K points per chunk: temporaries stay in cache
-    bounds = [(z, min(n, z + chunk)) for z in range(0, n, chunk)]
+    nd = blk.ndim
+    # memory axes from slowest to fastest
+    order = list(range(nd)) if blk.flags.c_contiguous else list(range(nd - 1, -1, -1))
+    snap = np.empty_like(blk)
+    ax0 = order[0]
+    nslow = blk.shape[ax0]
+    step0 = max(1, nslow // max(1, 4 * nthreads))
+
+    def copy(z0):
+        idx = [slice(None)] * nd
+        idx[ax0] = slice(z0, min(nslow, z0 + step0))
+        snap[tuple(idx)] = blk[tuple(idx)]
+
+    if pool is None or nthreads <= 1:
+        snap[...] = blk
+    else:
+        list(pool.map(copy, range(0, nslow, step0)))
+    # tiles of ~128K points: the fast axes whole, the slowest axis cut, and the next one
+    # too when one index of the slowest axis already holds more than that
+    target = 1 << 17
+
+    def cuts(n, c):
+        return [(z, min(n, z + c - 1)) for z in range(1, n + 1, c)]
+
+    ax_s = order[0]
+    inner = int(np.prod([shape[d] for d in order[1:]])) if nd > 1 else 1
+    tiles = []
+    for rs in cuts(shape[ax_s], max(1, target // inner)):
+        if nd > 2 and inner > target:
+            ax_t = order[1]
+            for rt in cuts(shape[ax_t], max(1, target // (inner // shape[ax_t]))):
+                t = [(1, m) for m in shape]
+                t[ax_s], t[ax_t] = rs, rt
+                tiles.append(t)
+        else:
+            t = [(1, m) for m in shape]
+            t[ax_s] = rs
+            tiles.append(t)
     name = kir.array_params[0]
 
-    def work(b):
-        z0, z1 = b
-        if z0 >= z1:
-            return
-        ranges = [(1, m) for m in shape]
-        ranges[ax] = (z0 + 1, z1)
-
+    def work(ranges):
         def read(_name, offsets):
             return snap[tuple(slice(a - 1 + h + o, e + h + o)
                               for (a, e), h, o in zip(ranges, lo, offsets))]
@@ -401,8 +430,8 @@ def threaded_machine_step(blk, lo, hi, kir, scalars=None, dtype=np.float64, pool
         blk[tuple(slice(a - 1 + h, e + h) for (a, e), h in zip(ranges, lo))] = pending[name]
 
     if pool is None or nthreads <= 1:
-        for b in bounds:
-            work(b)
+        for t in tiles:
+            work(t)
     else:
-        list(pool.map(work, bounds))
+        list(pool.map(work, tiles))
     return blk

@@ -22,7 +22,7 @@ DTYPES = {"f32": F32, "float32": F32, "f64": F64, "float64": F64}
 EXPORTS = ("lope_abi_version", "lope_last_error", "lope_set_cache_dir", "lope_layout_init",
            "lope_kernel_compile", "lope_kernel_destroy", "lope_kernel_describe",
            "lope_kernel_source", "lope_launch", "lope_step", "lope_step_planes", "lope_halo_fill", "lope_pack",
-           "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_kernel_prepare", "lope_step_multi",
+           "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_plan_set_variant", "lope_kernel_prepare", "lope_step_multi",
            "lope_step_planes_peer", "lope_ipc_export", "lope_ipc_open", "lope_ipc_close", "lope_copy_bytes",
            "lope_box_unpack", "lope_fill_hash", "lope_face_span", "lope_launch_count")
 
@@ -81,6 +81,7 @@ def lib():
     L.lope_plan_candidates.argtypes = [VP, P(I32), P(I32), P(I32), I32, P(I32)]
     L.lope_plan_set.argtypes = [VP, P(Layout), I32, I32, I32, I32]
     L.lope_plan_set_tile.argtypes = [VP, P(Layout), I32, P(I32), I32, I32, P(I32)]
+    L.lope_plan_set_variant.argtypes = [VP, P(Layout), I32, P(I32), I32, I32, P(I32)]
     L.lope_box_pack.argtypes = [P(Layout), VP, P(I64), P(I64), VP, VP]
     L.lope_box_unpack.argtypes = [P(Layout), VP, P(I64), P(I64), VP, VP]
     L.lope_fill_hash.argtypes = [P(Layout), VP, ctypes.c_uint64, P(I64), P(I64), VP]

@@ -1580,6 +1580,27 @@ int lope_plan_set_tile(lope_kernel* k, const lope_layout* layout, int32_t wrap_m
   return lope_plan_set(k, layout, wrap_mask, vi, zchunk, yband);
 }
 
+int lope_plan_set_variant(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, const int32_t* cfg,
+                          int32_t zchunk, int32_t yband, int32_t* variant) {
+  if (!k || !layout || !cfg) return fail(108, "null argument");
+  if (int e = check_layout(layout)) return e;
+  TileCfg c;
+  c.bxw = cfg[0];
+  c.wy = cfg[1];
+  c.ry = cfg[2];
+  c.ns = cfg[3];
+  c.pw = cfg[4] ? 1 : 0;
+  c.mb = cfg[5] == 2 ? 2 : 1;
+  c.sh = cfg[6] ? 1 : 0;
+  c.nb = cfg[7] ? 1 : 0;
+  if (c.bxw < 1 || c.wy < 1 || c.ry < 1 || c.ns < 2) return fail(108, "bad tile shape");
+  int vi = 0;
+  if (int e = add_variant(k, c, &vi)) return e;
+  if (!k->variants[vi].tiled_ok) return fail(108, "tile variant does not fit shared memory");
+  if (variant) *variant = vi;
+  return lope_plan_set(k, layout, wrap_mask, vi, zchunk, yband);
+}
+
 int lope_plan_set(lope_kernel* k, const lope_layout* layout, int32_t wrap_mask, int32_t variant, int32_t zchunk,
                   int32_t yband) {
   if (!k || !layout) return fail(108, "null argument");

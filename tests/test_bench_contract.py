@@ -22,7 +22,26 @@ def test_reference_arm_prints_one_contract_line():
     assert d["impl"] == "reference" and d["unit"] == "Gpoints/s" and d["higher_is_better"] is True
     assert d["config"]["workload"] == "c1" and d["value"] > 0
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    # config 1 is rank 2 and small: the reference's own Machine (baseline/_ref) is timed,
+    # on the full config for exactly the requested steps
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["config"]["same_config"] is True and cb["steps"] == d["steps"]
+    assert abs(d["ms_per_step"] * d["steps"] / 1e3 - cb["seconds"]) < 0.01
+
+
+def test_reference_arm_port_on_a_3d_config_states_its_sample():
+    """The port path (rank 3, which the reference Machine rejects): with a tight budget it
+    times a slab sample and says so (same_config false, measured ms_per_step)."""
+    import os
+    env = dict(os.environ, LOPE_BENCH_REF_BUDGET_S="3")
+    r = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--workload", "c3",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600,
+                       cwd=str(REPO), env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["same_config"] is False and "slab of the full" in cb["sample"]
+    assert d["config"]["same_config"] is False and d["value"] > 0
     assert d["e2e"] == {"value": d["value"], "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["gpu_launches"] == 0
