@@ -201,6 +201,57 @@ int lope_fill_hash(const lope_layout* layout, void* dev, uint64_t seed, const in
  * 3 last `lo` interior planes.  Used to exchange faces between slab partitions. */
 int lope_face_span(const lope_layout* layout, int32_t which, int64_t* offset, int64_t* count);
 
+/* ---- Halo exchange between GPUs: Machine._halo_exchange (runtime.py:643-711) for
+ * slab partitions (the slowest dim split over a ring of P images) ----
+ *
+ * One communicator per image (per process, or per host thread for ranks sharing a
+ * process).  Setup is transport-neutral: every rank exports a fixed-size record
+ * (lope_comm_record_size() bytes: its ping-pong buffers and step flags as CUDA IPC
+ * handles and raw pointers, and its block geometry), the caller gathers all P records
+ * in rank order over any out-of-band channel (torch.distributed, MPI, a file, shared
+ * memory) and hands them to lope_comm_connect, which maps the two ring neighbours.
+ *
+ *   lope_comm_step      one fused step: wait (stream memory op) until both neighbours
+ *                       finished their previous operation, ONE stencil kernel that
+ *                       stores the boundary planes' periodic images straight into the
+ *                       neighbours' output blocks over NVLink, then write this step's
+ *                       number into the neighbours' flags (system-scope fenced).
+ *   lope_halo_exchange  HALO_TRANSFER(U, BC=CYCLIC): local wrap of the other dims, then
+ *                       the neighbours' faces -- peer copies after a flag handshake, or
+ *                       ncclSend/ncclRecv in one group when only NCCL is initialised.
+ *   lope_comm_sync      order the stream after both neighbours' latest operation.
+ *
+ * All ranks run the same sequence of operations with the same live index (SPMD
+ * lockstep, as the reference's images do).  Errors: 201 bad image index / records
+ * from another grid, 108 non-uniform blocks or halo wider than a block (F8), 202
+ * missing setup, -3 transport unavailable. */
+typedef struct lope_comm lope_comm;
+
+int lope_comm_create(int32_t nranks, int32_t rank, lope_comm** out);
+int lope_comm_destroy(lope_comm* comm);
+int lope_comm_record_size(void);
+/* record: lope_comm_record_size() bytes written for this rank. */
+int lope_comm_export(lope_comm* comm, const lope_layout* layout, void* buf0, void* buf1, uint8_t* record);
+/* records: all P records, rank order, concatenated. */
+int lope_comm_connect(lope_comm* comm, const uint8_t* records);
+/* NCCL transport for lope_halo_exchange (NCCL is loaded at run time):
+ * rank 0 makes the 128-byte id, every rank passes it to lope_comm_nccl_init. */
+int lope_comm_nccl_unique_id(uint8_t* id);
+int lope_comm_nccl_init(lope_comm* comm, const uint8_t* id);
+/* transport: 1 peer, 2 NCCL, 0 none; epoch = synchronised operations so far. */
+int lope_comm_info(const lope_comm* comm, int32_t* rank, int32_t* nranks, uint32_t* epoch, int32_t* transport);
+/* dims_mask: bit d = dim d+1; the decomposed (slowest) dim's bit moves the faces
+ * between images, the other bits wrap locally (HALO_TRANSFER = all bits). */
+int lope_halo_exchange(lope_comm* comm, int32_t live, int32_t dims_mask, void* stream);
+/* The same in two phases (overlap, or ranks driven round-robin from one thread):
+ * _begin wraps the local dims and marks the block ready (NCCL: the whole exchange),
+ * _end waits for the neighbours' blocks and copies their faces. */
+int lope_halo_exchange_begin(lope_comm* comm, int32_t live, int32_t dims_mask, void* stream);
+int lope_halo_exchange_end(lope_comm* comm, void* stream);
+int lope_comm_step(lope_comm* comm, const lope_kernel* k, int32_t live, const double* rscal, const int64_t* iscal,
+                   void* stream);
+int lope_comm_sync(lope_comm* comm, void* stream);
+
 /* Number of this library's kernels launched since load (evidence for the bench). */
 int64_t lope_launch_count(void);
 

@@ -24,7 +24,11 @@ EXPORTS = ("lope_abi_version", "lope_last_error", "lope_set_cache_dir", "lope_la
            "lope_kernel_source", "lope_launch", "lope_step", "lope_step_planes", "lope_halo_fill", "lope_pack",
            "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_plan_set_variant", "lope_kernel_prepare", "lope_step_multi",
            "lope_step_planes_peer", "lope_ipc_export", "lope_ipc_open", "lope_ipc_close", "lope_copy_bytes",
-           "lope_box_unpack", "lope_fill_hash", "lope_face_span", "lope_launch_count")
+           "lope_box_unpack", "lope_fill_hash", "lope_face_span", "lope_launch_count",
+           "lope_comm_create", "lope_comm_destroy", "lope_comm_record_size", "lope_comm_export",
+           "lope_comm_connect", "lope_comm_nccl_unique_id", "lope_comm_nccl_init", "lope_comm_info",
+           "lope_halo_exchange", "lope_halo_exchange_begin", "lope_halo_exchange_end",
+           "lope_comm_step", "lope_comm_sync")
 
 
 class Layout(ctypes.Structure):
@@ -78,6 +82,19 @@ def lib():
     L.lope_ipc_close.argtypes = [VP]
     L.lope_copy_bytes.argtypes = [VP, VP, I64, VP]
     L.lope_step_multi.argtypes = [VP, P(Layout), VP, VP, I64, P(ctypes.c_double), P(I64), VP, P(I32)]
+    L.lope_comm_create.argtypes = [I32, I32, P(VP)]
+    L.lope_comm_destroy.argtypes = [VP]
+    L.lope_comm_record_size.restype = ctypes.c_int
+    L.lope_comm_export.argtypes = [VP, P(Layout), VP, VP, ctypes.c_char_p]
+    L.lope_comm_connect.argtypes = [VP, ctypes.c_char_p]
+    L.lope_comm_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.lope_comm_nccl_init.argtypes = [VP, ctypes.c_char_p]
+    L.lope_comm_info.argtypes = [VP, P(I32), P(I32), P(ctypes.c_uint32), P(I32)]
+    L.lope_halo_exchange.argtypes = [VP, I32, I32, VP]
+    L.lope_halo_exchange_begin.argtypes = [VP, I32, I32, VP]
+    L.lope_halo_exchange_end.argtypes = [VP, VP]
+    L.lope_comm_step.argtypes = [VP, VP, I32, P(ctypes.c_double), P(I64), VP]
+    L.lope_comm_sync.argtypes = [VP, VP]
     L.lope_plan_candidates.argtypes = [VP, P(I32), P(I32), P(I32), I32, P(I32)]
     L.lope_plan_set.argtypes = [VP, P(Layout), I32, I32, I32, I32]
     L.lope_plan_set_tile.argtypes = [VP, P(Layout), I32, P(I32), I32, I32, P(I32)]

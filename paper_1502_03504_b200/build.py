@@ -24,8 +24,9 @@ CACHE = PKG / "_jit_cache"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_LIB = "/usr/local/cuda/lib64"
 
-SOURCES = [CSRC / "lope_api.cu", CSRC / "lope_codegen.cpp"]
-DEPS = SOURCES + [CSRC / "lope_device.cuh", CSRC / "lope_codegen.h", REPO / "include" / "lope_b200.h"]
+SOURCES = [CSRC / "lope_api.cu", CSRC / "lope_comm.cu", CSRC / "lope_codegen.cpp"]
+DEPS = SOURCES + [CSRC / "lope_device.cuh", CSRC / "lope_codegen.h", CSRC / "lope_internal.h",
+                  REPO / "include" / "lope_b200.h"]
 
 
 def _gen_device_inc() -> pathlib.Path:
@@ -56,7 +57,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> pathlib.Path:
            "-I", str(REPO / "include"), "-I", str(CSRC),
            *[str(s) for s in SOURCES],
            "-o", str(LIB) + ".tmp",
-           "-L", CUDA_LIB, "-lnvrtc", "-Xlinker", f"-rpath,{CUDA_LIB}"]
+           "-L", CUDA_LIB, "-lnvrtc", "-ldl", "-Xlinker", f"-rpath,{CUDA_LIB}"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)

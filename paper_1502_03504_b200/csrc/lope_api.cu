@@ -32,6 +32,7 @@
 
 #include "../../include/lope_b200.h"
 #include "lope_codegen.h"
+#include "lope_internal.h"
 
 static const char* kDeviceSrc =
 #include "lope_device_src.inc"
@@ -157,6 +158,19 @@ int sm_count() {
 }
 
 }  // namespace
+
+// error reporting shared with the other translation units of the library (lope_internal.h)
+int lope_set_error(int code, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+void lope_count_launch() { g_launches++; }
 
 // ---------------------------------------------------------------------------
 // AOT kernels (nvcc, sm_100a)

@@ -732,21 +732,102 @@ class PeerMultiSlab:
             launch(self.kernel, [b], None, self.scalars)
 
 
-class PeerSlabStepper:
-    """Multi-GPU slabs with the exchange fused into the kernel (one process per GPU).
+class SlabComm:
+    """This image's communicator in liblope_b200.so (``lope_comm``, include/lope_b200.h).
 
-    At setup every rank exports both ping-pong buffers of its block (CUDA IPC) and
-    opens its two ring neighbours'.  A step is one kernel per rank that writes its
-    interior, the periodic images of the non-decomposed dims, and its boundary
-    planes' images directly into the neighbours' output blocks over NVLink; a
-    barrier then orders the step against the next one (the neighbours' halos are
-    complete, and nobody still reads the buffers the next step overwrites).  With
-    NCCL the barrier is a one-element all-reduce on the compute stream; with gloo
-    (tests) a device synchronise plus ``dist.barrier``.
+    The exchange of ``Machine._halo_exchange`` (runtime.py:643-711) between slab images
+    lives behind the C ABI: ``exchange`` (HALO_TRANSFER), ``step`` (one fused stencil
+    kernel whose epilogue stores the boundary planes' images into the neighbours' blocks,
+    ordered against the neighbours by stream memory operations on peer flags) and
+    ``sync``.  Python only moves the setup records between ranks (``gather``: any
+    all-gather of bytes in rank order; ``torch.distributed.all_gather_object`` for one
+    process per GPU) -- nothing in the step loop.
+    """
+
+    def __init__(self, block, rank: int, nranks: int):
+        block.spare()                        # both ping-pong buffers exist, fixed indices
+        self.block = block
+        self.rank, self.nranks = int(rank), int(nranks)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().lope_comm_create(self.nranks, self.rank, ctypes.byref(h)), "lope_comm_create")
+        self.handle = h.value
+
+    def export(self) -> bytes:
+        n = _lib.lib().lope_comm_record_size()
+        rec = ctypes.create_string_buffer(n)
+        b = self.block
+        _lib.check(_lib.lib().lope_comm_export(self.handle, ctypes.byref(b.layout),
+                                               ctypes.c_void_p(b._bufs[0].data_ptr()),
+                                               ctypes.c_void_p(b._bufs[1].data_ptr()), rec), "lope_comm_export")
+        return bytes(rec.raw)
+
+    def connect(self, records: Sequence[bytes]) -> None:
+        blob = b"".join(records)
+        _lib.check(_lib.lib().lope_comm_connect(self.handle, blob), "lope_comm_connect")
+
+    def nccl_init(self, uid: bytes) -> None:
+        _lib.check(_lib.lib().lope_comm_nccl_init(self.handle, uid), "lope_comm_nccl_init")
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(_lib.lib().lope_comm_nccl_unique_id(buf), "lope_comm_nccl_unique_id")
+        return bytes(buf.raw)
+
+    def info(self):
+        r, n, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        e = ctypes.c_uint32()
+        _lib.check(_lib.lib().lope_comm_info(self.handle, ctypes.byref(r), ctypes.byref(n), ctypes.byref(e),
+                                             ctypes.byref(t)), "lope_comm_info")
+        return {"rank": r.value, "nranks": n.value, "epoch": e.value,
+                "transport": {0: None, 1: "peer", 2: "nccl"}[t.value]}
+
+    def exchange(self, dims_mask: Optional[int] = None, stream=None, live: Optional[int] = None) -> None:
+        mask = (1 << self.block.rank) - 1 if dims_mask is None else dims_mask
+        _lib.check(_lib.lib().lope_halo_exchange(self.handle, self.block._live if live is None else live, mask,
+                                                 _stream_ptr(stream)), "lope_halo_exchange")
+
+    def exchange_begin(self, dims_mask: Optional[int] = None, stream=None) -> None:
+        mask = (1 << self.block.rank) - 1 if dims_mask is None else dims_mask
+        _lib.check(_lib.lib().lope_halo_exchange_begin(self.handle, self.block._live, mask, _stream_ptr(stream)),
+                   "lope_halo_exchange_begin")
+
+    def exchange_end(self, stream=None) -> None:
+        _lib.check(_lib.lib().lope_halo_exchange_end(self.handle, _stream_ptr(stream)), "lope_halo_exchange_end")
+
+    def step(self, kernel, rs, is_, stream=None) -> None:
+        _lib.check(_lib.lib().lope_comm_step(self.handle, kernel.handle, self.block._live, rs, is_,
+                                             _stream_ptr(stream)), "lope_comm_step")
+        self.block.swap()
+
+    def sync(self, stream=None) -> None:
+        _lib.check(_lib.lib().lope_comm_sync(self.handle, _stream_ptr(stream)), "lope_comm_sync")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.lib().lope_comm_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PeerSlabStepper:
+    """Multi-GPU slabs with the exchange fused into the kernel (one process per GPU),
+    through the C-ABI communicator (``SlabComm`` / ``lope_comm``).
+
+    A step is ``lope_comm_step``: a stream wait on the two neighbours' step flags, ONE
+    kernel that writes the slab's interior, the periodic images of the non-decomposed
+    dims and its boundary planes' images straight into the neighbours' output blocks
+    over NVLink, and the flag writes -- no collective and no host synchronisation.
+    ``torch.distributed`` only carries the setup records (all ranks agree: a rank that
+    cannot export or map makes every rank raise, and the caller falls back together).
     """
 
     def __init__(self, kernel, arr: SlabArray, scalars=None, group=None):
-        import torch
         import torch.distributed as dist
         self.kernel = kernel
         self.arr = arr
@@ -755,92 +836,44 @@ class PeerSlabStepper:
         self.dist = dist
         self._rs, self._is = kernel.scalar_args(scalars)
         blk = arr.block
-        blk.spare()
         self.rank, self.size = arr.rank, arr.size
-        self._nccl = dist.get_backend(group) == "nccl"
-        self._flag = torch.zeros(1, dtype=torch.int32, device=blk.data.device)
-        # Every step of the setup is agreed by all ranks: a rank that cannot export or
-        # map peer memory makes every rank raise (the caller then falls back to NCCL on
-        # all of them) instead of leaving the others waiting in a collective.
-        mine, why = [], None
+        self.comm, why = None, None
+        rec = None
         try:
-            for buf in blk._bufs:
-                h = ctypes.create_string_buffer(64)
-                off = ctypes.c_int64()
-                _lib.check(_lib.lib().lope_ipc_export(ctypes.c_void_p(buf.data_ptr()), h, ctypes.byref(off)),
-                           "lope_ipc_export")
-                mine.append((bytes(h.raw), int(off.value)))
+            self.comm = SlabComm(blk, self.rank, self.size)
+            rec = self.comm.export()
         except Exception as e:          # pragma: no cover - depends on the allocator
-            mine, why = None, repr(e)
-        allh = [None] * self.size
-        dist.all_gather_object(allh, mine, group=group)
-        if any(x is None for x in allh):
-            raise RuntimeError(f"peer memory export failed on some rank ({why or 'another rank'})")
-        prev, nxt = (self.rank - 1) % self.size, (self.rank + 1) % self.size
-        self._opened = []
-        self.peers = {}
-        ok = 1
-        try:
-            for who in sorted({prev, nxt}):
-                ptrs = []
-                for (h, off) in allh[who]:
-                    if who == self.rank:
-                        ptrs = [b.data_ptr() for b in blk._bufs]
-                        break
-                    p = ctypes.c_void_p()
-                    _lib.check(_lib.lib().lope_ipc_open(h, off, ctypes.byref(p)), "lope_ipc_open")
-                    self._opened.append(p.value)
-                    ptrs.append(p.value)
-                self.peers[who] = ptrs
-        except Exception as e:          # pragma: no cover - depends on the node
-            ok, why = 0, repr(e)
+            why = repr(e)
+        allr = [None] * self.size
+        dist.all_gather_object(allr, rec, group=group)
+        ok = 0
+        if all(r is not None for r in allr):
+            try:
+                self.comm.connect(allr)
+                ok = 1
+            except Exception as e:      # pragma: no cover - depends on the node
+                why = repr(e)
         flags = [None] * self.size
         dist.all_gather_object(flags, ok, group=group)
         if not all(flags):
-            self.close()                # unmap whatever was mapped
-            raise RuntimeError(f"peer memory mapping failed on some rank ({why or 'another rank'})")
-        self.prev, self.next = prev, nxt
-        d = arr.dim
-        L = blk.layout
-        self.m = int(L.interior[d])
+            self.close()
+            raise RuntimeError(f"peer mapping failed on some rank ({why or 'another rank'})")
         self.full = (1 << blk.rank) - 1
+        self.m = int(blk.layout.interior[arr.dim])
 
     def close(self) -> None:
-        for p in self._opened:
-            _lib.lib().lope_ipc_close(ctypes.c_void_p(p))
-        self._opened = []
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None
 
     def barrier(self) -> None:
-        import torch
-        if self._nccl:
-            self.dist.all_reduce(self._flag, group=self.group)     # stream-ordered
-        else:
-            torch.cuda.synchronize()
-            self.dist.barrier(group=self.group)
+        """Order this rank's stream after both neighbours' latest operation."""
+        self.comm.sync()
 
     def exchange(self) -> None:
         """``HALO_TRANSFER``: local dims wrap on the GPU, the decomposed dim's halo
-        planes are copied from the neighbours' live blocks through peer memory."""
-        from .runtime import halo_transfer
-        blk = self.arr.block
-        if self.size == 1:
-            halo_transfer(blk)
-            return
-        halo_transfer(blk, dims_mask=self.arr.local_mask)
-        self.barrier()
-        live = blk._live
-        eb = int(blk.layout.elem_bytes)
-        spans = {w: _lib.face_span(blk.layout, w) for w in range(4)}
-        base = blk.data.data_ptr()
-        # low halo <- previous image's last `lo` planes; high halo <- next image's first `hi`
-        for dst_w, who, src_w in ((0, self.prev, 3), (1, self.next, 2)):
-            off, cnt = spans[dst_w]
-            soff, _ = spans[src_w]
-            if cnt:
-                _lib.check(_lib.lib().lope_copy_bytes(ctypes.c_void_p(base + off * eb),
-                                                      ctypes.c_void_p(self.peers[who][live] + soff * eb),
-                                                      cnt * eb, _stream_ptr(None)), "lope_copy_bytes")
-        self.barrier()
+        planes are copied from the neighbours' live blocks (peer memory)."""
+        self.comm.exchange()
 
     def tune(self) -> int:
         """Run real steps until the plan for this block is chosen; returns the count."""
@@ -850,44 +883,14 @@ class PeerSlabStepper:
             n += 1
         return n
 
-    def kernel_ms_estimate(self, reps: int = 5) -> float:
-        """Average device time of the fused kernel over the whole slab (no barrier)."""
-        import torch
-        blk = self.arr.block
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        out = 1 - blk._live
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
-            _step_planes_peer(self.kernel, blk.layout, blk.data.data_ptr(), blk.spare().data_ptr(), 0, self.m,
-                              self._rs, self._is, self.full, self.peers[self.prev][out] if self.size > 1 else 0,
-                              self.peers[self.next][out] if self.size > 1 else 0, None)
-        e1.record()
-        torch.cuda.synchronize()
-        self.barrier()
-        return e0.elapsed_time(e1) / reps
-
     def step(self) -> None:
         blk = self.arr.block
-        if self.size == 1:
-            from .runtime import step
-            step(self.kernel, blk, self.scalars)
-            return
         tuner = self.kernel.tuner(blk, self.full)
         if tuner is not None:
             tuner.before()
-        self._step()
+        self.comm.step(self.kernel, self._rs, self._is)
         if tuner is not None:
             tuner.after()
-
-    def _step(self) -> None:
-        blk = self.arr.block
-        out = 1 - blk._live
-        _step_planes_peer(self.kernel, blk.layout, blk.data.data_ptr(), blk.spare().data_ptr(), 0, self.m,
-                          self._rs, self._is, self.full, self.peers[self.prev][out], self.peers[self.next][out],
-                          None)
-        blk.swap()
-        self.barrier()
 
     def iterate(self, steps: int) -> None:
         from .runtime import launch
@@ -896,4 +899,72 @@ class PeerSlabStepper:
         self.exchange()
         for _ in range(steps - 1):
             self.step()
+        self.comm.sync()
         launch(self.kernel, [self.arr.block], None, self.scalars)
+
+
+class CommMultiSlab:
+    """P slab images in ONE process, each with its own ``lope_comm`` and CUDA stream,
+    connected through raw pointers: the C-ABI exchange and fused-step protocol (flags,
+    stream waits, peer stores) exercised end to end on one GPU.
+
+    Nothing here waits inside a kernel: the waits are stream memory operations, and the
+    operations are enqueued round by round (every image's operation k before any image's
+    operation k+1), so each wait's signal is enqueued before it -- no order of the
+    streams on the hardware queues can deadlock.  Run it with
+    ``CUDA_DEVICE_MAX_CONNECTIONS`` >= P + 1 so the streams do not share a queue.
+    """
+
+    def __init__(self, kernel, global_shape, lo, hi, dtype, nranks: int, scalars=None):
+        import torch
+        from .runtime import HaloArray
+        self.grid = SlabGrid(global_shape, nranks, lo, hi)
+        self.kernel = kernel
+        self.scalars = scalars
+        self.blocks = [HaloArray(self.grid.local_shape, lo, hi, dtype) for _ in range(nranks)]
+        self.streams = [torch.cuda.Stream() for _ in range(nranks)]
+        torch.cuda.synchronize()
+        self.comms = [SlabComm(b, r, nranks) for r, b in enumerate(self.blocks)]
+        torch.cuda.synchronize()
+        recs = [c.export() for c in self.comms]
+        for c in self.comms:
+            c.connect(recs)
+        self._rs, self._is = kernel.scalar_args(scalars)
+        self.dim = len(global_shape) - 1
+
+    set_global = MultiSlab.set_global
+    get_global = MultiSlab.get_global
+
+    def _all(self, fn):
+        import torch
+        for c, s in zip(self.comms, self.streams):
+            with torch.cuda.stream(s):
+                fn(c, s)
+
+    def halo_transfer(self) -> None:
+        # two rounds: every image's "ready" signal is enqueued before any image waits
+        self._all(lambda c, s: c.exchange_begin(stream=s))
+        self._all(lambda c, s: c.exchange_end(stream=s))
+
+    def step(self) -> None:
+        self._all(lambda c, s: c.step(self.kernel, self._rs, self._is, stream=s))
+
+    def iterate(self, steps: int) -> None:
+        import torch
+        from .runtime import launch
+        if steps <= 0:
+            return
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        self.halo_transfer()
+        for _ in range(steps - 1):
+            self.step()
+        self._all(lambda c, s: c.sync(stream=s))
+        self._all(lambda c, s: launch(self.kernel, [c.block], None, self.scalars, stream=s))
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def close(self) -> None:
+        for c in self.comms:
+            c.close()

@@ -3,6 +3,7 @@
 
     python tools/ncu_traffic.py --workload c3 --from-bench gpurun_out/bench.jsonl
     python tools/ncu_traffic.py --workload c3 --plan 1,16,2,8,1,1,1,0:8
+    python tools/ncu_traffic.py --merge gpurun_out/traffic_c3.json ...   # here, afterwards
 
 Runs ``bench.py`` with the plan replayed (``--plan``: no tuning, so the profiled
 launches are the plan's) under
@@ -55,6 +56,19 @@ def parse_plan(arg):
 
 
 def main():
+    if len(sys.argv) > 2 and sys.argv[1] == "--merge":
+        # here, after a GPU session: the entries the box printed (its profiles/ is not copied back)
+        ents = []
+        for f in sys.argv[2:]:
+            for line in pathlib.Path(f).read_text().splitlines():
+                if line.startswith("{"):
+                    e = json.loads(line)
+                    if e.get("ncu_kernel_ms", 0) > 1e4:           # entries written before the ns fix
+                        e["ncu_kernel_ms"] = round(e["ncu_kernel_ms"] / 1e6, 4)
+                    ents.append(e)
+        merge(ents)
+        print(f"merged {len(ents)} entr{'y' if len(ents) == 1 else 'ies'}")
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", required=True)
     ap.add_argument("--plan")
@@ -86,7 +100,7 @@ def main():
         unit = row.get("Metric Unit", "")
         v = float(row["Metric Value"].replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
-                 "msecond": 1.0}.get(unit, 1.0)
+                 "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(unit, 1.0)
         vals.setdefault(row["Metric Name"], []).append(v * scale)
     rd = statistics.median(vals["dram__bytes_read.sum"])
     wr = statistics.median(vals["dram__bytes_write.sum"])
@@ -97,14 +111,20 @@ def main():
              "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                        f"--clock-control none --cache-control none, median of {len(vals['dram__bytes_read.sum'])} "
                        f"{a.kernel} launches after {a.skip}, bench.py --workload {a.workload} --plan {plan}"}
+    merge([entry])
+    print(json.dumps(entry))
+
+
+def merge(entries):
+    """Add entries to profiles/ncu_traffic.json (replacing the same workload + plan)."""
     p = REPO / "profiles" / "ncu_traffic.json"
     d = json.loads(p.read_text()) if p.exists() else {}
     if "entries" not in d:
         d = {"entries": [], "round1": d}
-    d["entries"] = [e for e in d["entries"]
-                    if not (e["workload"] == a.workload and e["plan"] == entry["plan"])] + [entry]
+    for entry in entries:
+        d["entries"] = [e for e in d["entries"]
+                        if not (e["workload"] == entry["workload"] and e["plan"] == entry["plan"])] + [entry]
     p.write_text(json.dumps(d, indent=1) + "\n")
-    print(json.dumps(entry))
 
 
 if __name__ == "__main__":
