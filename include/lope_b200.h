@@ -238,7 +238,10 @@ int lope_comm_connect(lope_comm* comm, const uint8_t* records);
  * rank 0 makes the 128-byte id, every rank passes it to lope_comm_nccl_init. */
 int lope_comm_nccl_unique_id(uint8_t* id);
 int lope_comm_nccl_init(lope_comm* comm, const uint8_t* id);
-/* transport: 1 peer, 2 NCCL, 0 none; epoch = synchronised operations so far. */
+/* transport: 1 peer, 2 NCCL, 0 none, 3 peer with host ordering (a neighbour is another
+ * process on the same GPU: the flags are not used -- ranks sharing a GPU must not wait on
+ * each other on the device -- and the caller orders every operation on the host, e.g. a
+ * device synchronise and a barrier); epoch = synchronised operations so far. */
 int lope_comm_info(const lope_comm* comm, int32_t* rank, int32_t* nranks, uint32_t* epoch, int32_t* transport);
 /* dims_mask: bit d = dim d+1; the decomposed (slowest) dim's bit moves the faces
  * between images, the other bits wrap locally (HALO_TRANSFER = all bits). */

@@ -156,6 +156,7 @@ struct Record {
   int64_t off_buf[2], off_flags;      // offsets of the pointers inside their allocations
   int32_t has_ipc;
   int32_t pad;
+  char bus[32];                       // PCI bus id of the device: ranks of two processes on one GPU
 };
 
 }  // namespace
@@ -170,6 +171,10 @@ struct lope_comm {
   int32_t* nb_flags[2] = {nullptr, nullptr};
   std::vector<void*> opened;            // IPC mappings to close (the pointers lope_ipc_open returned)
   uint32_t epoch = 0;                   // completed synchronised operations
+  // Neighbours in another process on the SAME GPU: their stream waits would block each
+  // other's contexts (B200_PROFILING.md: ranks sharing a GPU must not wait on one another),
+  // so the flags are not used and the caller orders the operations on the host.
+  bool host_ordered = false;
   uint32_t pending = 0;                 // signalled exchange awaiting lope_halo_exchange_end
   int pending_live = 0;
   ncclComm_t nccl = nullptr;
@@ -189,7 +194,7 @@ int check_stream_memops() {
 
 // this rank finished operation `v`: tell both neighbours (their flag slot for us)
 int signal(lope_comm* c, uint32_t v, cudaStream_t st) {
-  if (c->nranks == 1) return 0;
+  if (c->nranks == 1 || c->host_ordered) return 0;
   if (int e = check_stream_memops()) return e;
   // prev's slot [1] is written by its next neighbour (us); next's slot [0] by its prev (us)
   int32_t* targets[2] = {c->nb_flags[0] + 1, c->nb_flags[1] + 0};
@@ -202,7 +207,7 @@ int signal(lope_comm* c, uint32_t v, cudaStream_t st) {
 
 // wait (on the stream) until both neighbours have signalled at least `v`
 int wait_for(lope_comm* c, uint32_t v, cudaStream_t st) {
-  if (c->nranks == 1 || v == 0) return 0;
+  if (c->nranks == 1 || v == 0 || c->host_ordered) return 0;
   if (int e = check_stream_memops()) return e;
   for (int i = 0; i < 2; ++i) {
     CUresult r = memops().wait((CUstream)st, (CUdeviceptr)(c->flags + i), v, CU_STREAM_WAIT_VALUE_GEQ);
@@ -281,6 +286,7 @@ int lope_comm_export(lope_comm* c, const lope_layout* layout, void* buf0, void* 
   r.raw_buf[1] = (uint64_t)(uintptr_t)buf1;
   r.raw_flags = (uint64_t)(uintptr_t)c->flags;
   r.has_ipc = 0;
+  if (cudaDeviceGetPCIBusId(r.bus, (int)sizeof r.bus - 1, c->device) != cudaSuccess) r.bus[0] = 0;
   if (c->nranks > 1 && !std::getenv("LOPE_COMM_NO_IPC")) {
     // IPC handles for neighbours in other processes (ranks of this process use raw pointers)
     if (export_ptr(buf0, r.ipc_buf[0], &r.off_buf[0]) == 0 && export_ptr(buf1, r.ipc_buf[1], &r.off_buf[1]) == 0 &&
@@ -338,6 +344,7 @@ int lope_comm_connect(lope_comm* c, const uint8_t* records) {
       }
       if (!r.has_ipc) return lope_set_error(-3, "image %d exported no IPC handles", nb[s] + 1);
       if (r.host != c->mine.host) return lope_set_error(-3, "image %d is on another node", nb[s] + 1);
+      if (r.bus[0] && std::strncmp(r.bus, c->mine.bus, sizeof r.bus) == 0) c->host_ordered = true;
       void* p = nullptr;
       for (int b = 0; b < 2; ++b) {
         if (int e = lope_ipc_open(r.ipc_buf[b], r.off_buf[b], &p)) return e;
@@ -384,7 +391,7 @@ int lope_comm_info(const lope_comm* c, int32_t* rank, int32_t* nranks, uint32_t*
   if (rank) *rank = c->rank;
   if (nranks) *nranks = c->nranks;
   if (epoch) *epoch = c->epoch;
-  if (transport) *transport = c->connected ? 1 : (c->nccl ? 2 : 0);
+  if (transport) *transport = c->connected ? (c->host_ordered ? 3 : 1) : (c->nccl ? 2 : 0);
   return 0;
 }
 

@@ -184,9 +184,15 @@ class SlabArray:
 
 
 class SlabStepper:
-    """Fused step on a slab: boundary planes, NCCL face exchange || interior planes."""
+    """Fused step on a slab: boundary planes, NCCL face exchange || interior planes.
 
-    def __init__(self, kernel, arr: SlabArray, scalars=None, overlap: bool = True):
+    With ``native=True`` (one process per GPU, NCCL) the faces travel through the C-ABI
+    communicator's NCCL transport (``lope_halo_exchange``: ncclSend/ncclRecv of the
+    contiguous faces in one group on the communication stream); otherwise through
+    ``torch.distributed`` (``NcclExchanger``, also the gloo path of the CPU tests)."""
+
+    def __init__(self, kernel, arr: SlabArray, scalars=None, overlap: bool = True, native: bool = False,
+                 group=None):
         import torch
         self.kernel = kernel
         self.arr = arr
@@ -194,6 +200,16 @@ class SlabStepper:
         self.overlap = overlap
         self.comm = torch.cuda.Stream() if overlap else None
         self._rs, self._is = kernel.scalar_args(scalars)
+        self.native = None
+        if native and arr.size > 1:
+            import torch.distributed as dist
+            c = SlabComm(arr.block, arr.rank, arr.size)
+            c.export()
+            uid = [SlabComm.nccl_unique_id() if arr.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            c.nccl_init(uid[0])
+            self.native = c
         L = arr.block.layout
         d = arr.dim
         self.m = int(L.interior[d])
@@ -237,17 +253,24 @@ class SlabStepper:
         b_hi_beg = max(m - lo, b_lo_end)    # last `lo` planes  -> next image
         self._planes(src, dst, 0, b_lo_end, cs)
         self._planes(src, dst, b_hi_beg, m, cs)
+        d_bit = 1 << self.arr.dim
         if self.overlap:
             ev = torch.cuda.Event()
             ev.record(cs)
             self.comm.wait_event(ev)
-            self.arr.exchanger.exchange(dst, blk.layout, self.comm)
+            if self.native is not None:
+                self.native.exchange(d_bit, self.comm, live=1 - blk._live)
+            else:
+                self.arr.exchanger.exchange(dst, blk.layout, self.comm)
             self._planes(src, dst, b_lo_end, b_hi_beg, cs)
             done = torch.cuda.Event()
             done.record(self.comm)
             cs.wait_event(done)
         else:
-            self.arr.exchanger.exchange(dst, blk.layout, cs)
+            if self.native is not None:
+                self.native.exchange(d_bit, cs, live=1 - blk._live)
+            else:
+                self.arr.exchanger.exchange(dst, blk.layout, cs)
             self._planes(src, dst, b_lo_end, b_hi_beg, cs)
         blk.swap()
 
@@ -780,7 +803,7 @@ class SlabComm:
         _lib.check(_lib.lib().lope_comm_info(self.handle, ctypes.byref(r), ctypes.byref(n), ctypes.byref(e),
                                              ctypes.byref(t)), "lope_comm_info")
         return {"rank": r.value, "nranks": n.value, "epoch": e.value,
-                "transport": {0: None, 1: "peer", 2: "nccl"}[t.value]}
+                "transport": {0: None, 1: "peer", 2: "nccl", 3: "peer-host-ordered"}[t.value]}
 
     def exchange(self, dims_mask: Optional[int] = None, stream=None, live: Optional[int] = None) -> None:
         mask = (1 << self.block.rank) - 1 if dims_mask is None else dims_mask
@@ -860,20 +883,33 @@ class PeerSlabStepper:
             raise RuntimeError(f"peer mapping failed on some rank ({why or 'another rank'})")
         self.full = (1 << blk.rank) - 1
         self.m = int(blk.layout.interior[arr.dim])
+        # two processes on one GPU (tests): no device-side waits between them, the host
+        # orders every operation instead (synchronise + barrier)
+        self.host_ordered = self.comm.info()["transport"] == "peer-host-ordered"
 
     def close(self) -> None:
         if self.comm is not None:
             self.comm.close()
             self.comm = None
 
+    def _host_order(self) -> None:
+        if self.host_ordered:
+            import torch
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+
     def barrier(self) -> None:
         """Order this rank's stream after both neighbours' latest operation."""
         self.comm.sync()
+        self._host_order()
 
     def exchange(self) -> None:
         """``HALO_TRANSFER``: local dims wrap on the GPU, the decomposed dim's halo
         planes are copied from the neighbours' live blocks (peer memory)."""
-        self.comm.exchange()
+        self.comm.exchange_begin()
+        self._host_order()
+        self.comm.exchange_end()
+        self._host_order()
 
     def tune(self) -> int:
         """Run real steps until the plan for this block is chosen; returns the count."""
@@ -889,6 +925,7 @@ class PeerSlabStepper:
         if tuner is not None:
             tuner.before()
         self.comm.step(self.kernel, self._rs, self._is)
+        self._host_order()
         if tuner is not None:
             tuner.after()
 
@@ -899,7 +936,7 @@ class PeerSlabStepper:
         self.exchange()
         for _ in range(steps - 1):
             self.step()
-        self.comm.sync()
+        self.barrier()
         launch(self.kernel, [self.arr.block], None, self.scalars)
 
 

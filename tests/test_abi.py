@@ -195,3 +195,31 @@ def test_boundary_rejects_bad_calls_with_reference_codes():
         assert L.lope_launch(h, ctypes.byref(lay), (ctypes.c_int64 * 6)(*rng), ins, outs, rs, is_, None) == 108, rng
     assert b"" != L.lope_last_error()
     _lib.destroy_kernel(h)
+
+
+def test_comm_boundary_checks_without_a_gpu():
+    """lope_comm's argument and setup-order checks (no device work): the reference's
+    E-codes for a bad image index (E201) and missing setup (E202)."""
+    import ctypes
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    assert L.lope_comm_create(0, 0, ctypes.byref(h)) == 201
+    assert L.lope_comm_create(4, 4, ctypes.byref(h)) == 201
+    assert L.lope_comm_create(4, -1, ctypes.byref(h)) == 201
+    assert L.lope_comm_create(4, 1, ctypes.byref(h)) == 0 and h.value
+    assert L.lope_comm_record_size() >= 256
+    recs = ctypes.create_string_buffer(4 * L.lope_comm_record_size())
+    assert L.lope_comm_connect(h, recs) == 202                      # export first
+    assert L.lope_halo_exchange(h, 0, 7, None) == 202
+    assert L.lope_comm_step(h, ctypes.c_void_p(0x10), 0, None, None, None) == 202
+    lay = _lib.make_layout(3, "f32", (64, 32, 16), (1, 1, 1), (1, 1, 1))
+    assert L.lope_comm_export(h, ctypes.byref(lay), None, None, recs) == 202
+    A = ctypes.c_void_p(0x1000)
+    assert L.lope_comm_export(h, ctypes.byref(lay), A, A, recs) == 108   # same buffer twice
+    thin = _lib.make_layout(3, "f32", (64, 32, 1), (1, 1, 2), (1, 1, 2))
+    assert L.lope_comm_export(h, ctypes.byref(thin), A, ctypes.c_void_p(0x2000), recs) == 108   # F8
+    r, n, e, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint32(), ctypes.c_int32()
+    assert L.lope_comm_info(h, ctypes.byref(r), ctypes.byref(n), ctypes.byref(e), ctypes.byref(t)) == 0
+    assert (r.value, n.value, e.value, t.value) == (1, 4, 0, 0)
+    assert L.lope_halo_exchange_end(h, None) == 0                   # nothing pending
+    assert L.lope_comm_destroy(h) == 0
