@@ -103,9 +103,16 @@ template <> struct LopeAr<double> {
       const double q = __dmul_rn(x, y);
       const double r = __fma_rn(-q, b, x);
       const double m = __fma_rn(r, y, q);
+#ifndef LOPE_DIVC_DSETP
+      bool inr, special;
+      classify(x, inr, special);
+      slow |= (y != y) || !(inr | special);
+      return inr ? m : q;
+#else
       const bool special = !(ax > 0.0 && ax <= 0x1.fffffffffffffp+1023);
       slow |= (y != y) || (!special && !(ax >= 0x1p-900 && ax <= 0x1p+900));
       return special ? q : m;
+#endif
     }
     if (y == y && ax >= 0x1p-900 && ax <= 0x1p+900) {
       const double q = __dmul_rn(x, y);
@@ -113,6 +120,16 @@ template <> struct LopeAr<double> {
       return __fma_rn(r, y, q);
     }
     return __ddiv_rn(x, b);
+  }
+  // Range classification of a dividend from its exponent bits, on the integer pipe:
+  // the fp64 pipe (DSETP) is the one the stencil's adds saturate (config 4: 24 DADD per
+  // point).  in_range: 2^-900 <= |x| < 2^900, where the FMA-corrected quotient is exact;
+  // special: +-0, +-inf, NaN, where q = x*y already has IEEE division's bits.
+  static __device__ __forceinline__ void classify(double x, bool& in_range, bool& special) {
+    const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+    const unsigned e = (hi >> 20) & 0x7ffu;
+    in_range = (e - 123u) <= 1798u;
+    special = e == 0x7ffu || ((hi & 0x7fffffffu) | lo) == 0u;
   }
   template <bool FAST>
   static __device__ __forceinline__ double divc(double x, double b, double, double yd, bool, bool ok, bool& slow) {
@@ -122,9 +139,16 @@ template <> struct LopeAr<double> {
       const double q = __dmul_rn(x, yd);
       const double r = __fma_rn(-q, b, x);
       const double m = __fma_rn(r, yd, q);
+#ifndef LOPE_DIVC_DSETP
+      bool inr, special;
+      classify(x, inr, special);
+      slow |= !(inr | special);
+      return inr ? m : q;
+#else
       const bool special = !(ax > 0.0 && ax <= 0x1.fffffffffffffp+1023);
       slow |= !special && !(ax >= 0x1p-900 && ax <= 0x1p+900);
       return special ? q : m;
+#endif
     }
     if (ax >= 0x1p-900 && ax <= 0x1p+900) {
       const double q = __dmul_rn(x, yd);
@@ -294,8 +318,56 @@ __device__ __forceinline__ void lope_mbar_expect_tx(lope_u64* bar, lope_u32 byte
 #if !defined(LOPE_WAIT_HINT_NS) && !defined(LOPE_NO_WAIT_HINT)
 #define LOPE_WAIT_HINT_NS 5000
 #endif
+// Shared-window address of a barrier (computed once per kernel; the generic-to-shared
+// conversion costs an S2R + LEA when left inside the plane loop).
+__device__ __forceinline__ bool lope_mbar_test_addr(lope_u32 addr, lope_u32 parity) {
+  lope_u32 done = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void lope_mbar_wait_slow(lope_u32 addr, lope_u32 parity);
+// Fast path: one non-blocking probe (the phase has usually completed -- the producer
+// runs NS-HOLD planes ahead); only a miss enters the suspending, bounded wait loop.
+__device__ __forceinline__ void lope_mbar_wait_addr(lope_u32 addr, lope_u32 parity) {
+  if (!lope_mbar_test_addr(addr, parity)) lope_mbar_wait_slow(addr, parity);
+}
+__device__ __forceinline__ void lope_mbar_arrive_addr(lope_u32 addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
   const lope_u32 addr = lope_smem_u32(bar);
+  lope_u32 done = 0, n = 0;
+  do {
+#ifdef LOPE_WAIT_HINT_NS
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "n"(LOPE_WAIT_HINT_NS)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+#endif
+    if (++n > LOPE_WAIT_LIMIT) __trap();
+  } while (!done);
+}
+// The bounded, suspending loop of lope_mbar_wait_addr: a TMA that never lands traps
+// (kernel error) instead of hanging the GPU.  (Inline: a call would make the compiler
+// save the live register window to local memory around it.)
+__device__ __forceinline__ void lope_mbar_wait_slow(lope_u32 addr, lope_u32 parity) {
   lope_u32 done = 0, n = 0;
   do {
 #ifdef LOPE_WAIT_HINT_NS
@@ -514,11 +586,13 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
   // Loads below `needed` are waited for (the issuing warp reads them next); loads up to
   // `limit` are prefetch and only issued while their slot is already free, so the
   // in-band producer never stalls warp 0 on a slower warp just to run further ahead.
+  int p_slot = 0;
+  lope_u32 p_round = 0;     // p_L = p_round * NS + p_slot, kept without division
   auto produce = [&](lope_u32 needed, lope_u32 limit) {
     while (p_L < limit && p_u < nunits) {
-      const lope_u32 slot = p_L % NS;
-      if (p_L >= (lope_u32)NS) {
-        const lope_u32 par = ((p_L / NS) - 1) & 1;
+      const int slot = p_slot;
+      if (p_round > 0) {
+        const lope_u32 par = (p_round - 1) & 1;
         if (p_L < needed) lope_mbar_wait(&empty[slot], par);
         else if (!lope_mbar_test(&empty[slot], par)) break;
       }
@@ -528,6 +602,7 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
       else
         lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by, p_z + p_pl);
       ++p_L;
+      if (++p_slot == NS) { p_slot = 0; ++p_round; }
       if (++p_pl == p_nl) {
         p_pl = 0;
         p_u += gridDim.x;
@@ -563,8 +638,14 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
 
   LopeUnitWalk w;
   w.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
-  lope_u32 lbase = 0;
   T hist[FZN > 0 ? FZN : 1][RY][VX];
+  // Ring position of the window's first plane, tracked incrementally (slot, phase) so
+  // the plane loop does no division by the ring depth; barrier addresses in the shared
+  // window are formed once.
+  const lope_u32 full_a = lope_smem_u32(full), empty_a = lope_smem_u32(empty);
+  int c_slot = 0;
+  lope_u32 c_par = 0;
+  lope_u32 lbase = 0;     // (the in-band producer's "needed" bound)
   for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
     const int z0 = w.zi * zc;
     const int nz = min(zc, g.ext[2] - z0);
@@ -592,20 +673,28 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
         __syncwarp();
       }
       // ---- wait for the planes this iteration reads ----
+      // The window slides by one plane: after the unit's first plane only the newest
+      // plane has not been waited for (a slot cannot be refilled while this warp holds
+      // it, so an earlier completed phase stays complete).
       const T* sp[NZW];
+      int ks[NZW];
+      lope_u32 kp[NZW];
 #pragma unroll
       for (int k = 0; k < NZW; ++k) {
-        const lope_u32 L = lbase + pz + k;
-        sp[k] = reinterpret_cast<const T*>(lope_smem + (L % NS) * C::STAGE_BYTES) + soff;
-        if (ZHIST && k < FZN && pz > 0) continue;          // past planes come from registers
-        lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+        int sl = c_slot + k;
+        lope_u32 ph = c_par;
+        if (sl >= NS) { sl -= NS; ph ^= 1u; }
+        ks[k] = sl;
+        kp[k] = ph;
+        sp[k] = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
+        const bool need = pz == 0 ? !(ZHIST && k < FZN) : (k == NZW - 1);
+        if (need) lope_mbar_wait_addr(full_a + 8u * sl, ph);
       }
       if (ZHIST && pz == 0) {
         // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
 #pragma unroll
         for (int d = 0; d < FZN; ++d) {
-          const lope_u32 L = lbase + (FZN - 1 - d);
-          lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+          lope_mbar_wait_addr(full_a + 8u * ks[FZN - 1 - d], kp[FZN - 1 - d]);
 #pragma unroll
           for (int r = 0; r < RY; ++r) {
             const V vv = *reinterpret_cast<const V*>(sp[FZN - 1 - d] + (Body::FN1 + r) * C::BOXX);
@@ -722,16 +811,21 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
       if (lane == 0) {
         if (ZHIST) {
           if (pz == 0)
-            for (int k = 0; k < FZN; ++k) lope_mbar_arrive(&empty[(lbase + k) % NS]);
-          lope_mbar_arrive(&empty[(lbase + pz + FZN) % NS]);
+#pragma unroll
+            for (int k = 0; k < FZN; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[k]);
+          lope_mbar_arrive_addr(empty_a + 8u * ks[FZN]);
           if (pz == nz - 1)
-            for (int k = 1; k <= FZP; ++k) lope_mbar_arrive(&empty[(lbase + pz + FZN + k) % NS]);
+#pragma unroll
+            for (int k = 1; k <= FZP; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[FZN + k]);
         } else {
-          lope_mbar_arrive(&empty[(lbase + pz) % NS]);
+          lope_mbar_arrive_addr(empty_a + 8u * ks[0]);
           if (pz == nz - 1)
-            for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
+#pragma unroll
+            for (int k = 1; k < NZW; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[k]);
         }
       }
+      // the window's first plane moves on by one
+      if (++c_slot == NS) { c_slot = 0; c_par ^= 1u; }
       if (!xok || nrow <= 0) continue;
       // ---- store ----
       const int zg = z0 + pz + g.r0[2];
@@ -783,6 +877,10 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
       }
     }
     lbase += nz + NZW - 1;
+    // the next unit's window starts NZW - 1 planes further (this unit's trailing halo)
+#pragma unroll
+    for (int k = 0; k < NZW - 1; ++k)
+      if (++c_slot == NS) { c_slot = 0; c_par ^= 1u; }
   }
 }
 
