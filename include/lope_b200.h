@@ -227,6 +227,11 @@ int lope_face_span(const lope_layout* layout, int32_t which, int64_t* offset, in
  * missing setup, -3 transport unavailable. */
 typedef struct lope_comm lope_comm;
 
+/* Let the current device read/write `peer_device`'s memory (NVLink P2P); no-op for the
+ * device itself or when already enabled.  The drop-in Machine's images on several GPUs
+ * of one process copy halo slabs through it. */
+int lope_peer_enable(int32_t peer_device);
+
 int lope_comm_create(int32_t nranks, int32_t rank, lope_comm** out);
 int lope_comm_destroy(lope_comm* comm);
 int lope_comm_record_size(void);

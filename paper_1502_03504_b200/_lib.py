@@ -28,7 +28,7 @@ EXPORTS = ("lope_abi_version", "lope_last_error", "lope_set_cache_dir", "lope_la
            "lope_comm_create", "lope_comm_destroy", "lope_comm_record_size", "lope_comm_export",
            "lope_comm_connect", "lope_comm_nccl_unique_id", "lope_comm_nccl_init", "lope_comm_info",
            "lope_halo_exchange", "lope_halo_exchange_begin", "lope_halo_exchange_end",
-           "lope_comm_step", "lope_comm_sync")
+           "lope_comm_step", "lope_comm_sync", "lope_peer_enable")
 
 
 class Layout(ctypes.Structure):
@@ -95,6 +95,7 @@ def lib():
     L.lope_halo_exchange_end.argtypes = [VP, VP]
     L.lope_comm_step.argtypes = [VP, VP, I32, P(ctypes.c_double), P(I64), VP]
     L.lope_comm_sync.argtypes = [VP, VP]
+    L.lope_peer_enable.argtypes = [I32]
     L.lope_plan_candidates.argtypes = [VP, P(I32), P(I32), P(I32), I32, P(I32)]
     L.lope_plan_set.argtypes = [VP, P(Layout), I32, I32, I32, I32]
     L.lope_plan_set_tile.argtypes = [VP, P(Layout), I32, P(I32), I32, I32, P(I32)]

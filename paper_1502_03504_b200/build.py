@@ -88,10 +88,31 @@ def precompile_kernels() -> list:
     return done
 
 
+REFERENCE = pathlib.Path("/root/reference/pkg")
+SUITE = REPO / "baseline" / "_ref" / "reference_suite"
+
+
+def stage_reference_suite() -> bool:
+    """Copy the reference's own test suite and corpus next to its installed package
+    (baseline/_ref/reference_suite: git-ignored, travels to the GPU box like the .so),
+    so tests/test_gpu_reference_suite.py can re-run it against the GPU Machine.  Only
+    here, where /root/reference exists; it is test infrastructure, never product."""
+    import shutil
+    if not (REFERENCE / "tests").is_dir():
+        return SUITE.is_dir()
+    for sub in ("tests", "corpus"):
+        dst = SUITE / sub
+        if dst.exists():
+            shutil.rmtree(dst)
+        shutil.copytree(REFERENCE / sub, dst, ignore=shutil.ignore_patterns("__pycache__", "*.pyc"))
+    return True
+
+
 def main() -> None:
     build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print("built", LIB)
     print("precompiled", ", ".join(precompile_kernels()))
+    print("reference suite staged:", stage_reference_suite())
 
 
 if __name__ == "__main__":

@@ -226,6 +226,23 @@ extern "C" {
 
 int lope_comm_record_size(void) { return (int)sizeof(Record); }
 
+int lope_peer_enable(int32_t peer_device) {
+  int cur = 0;
+  COMM_CUDA_TRY(cudaGetDevice(&cur));
+  if (peer_device == cur) return 0;
+  int can = 0;
+  COMM_CUDA_TRY(cudaDeviceCanAccessPeer(&can, cur, peer_device));
+  if (!can) return lope_set_error(-3, "device %d cannot access device %d's memory (no P2P)", cur, peer_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (e != cudaSuccess) return lope_set_error(-(int)e, "cudaDeviceEnablePeerAccess(%d): %s", peer_device,
+                                              cudaGetErrorString(e));
+  return 0;
+}
+
 int lope_comm_create(int32_t nranks, int32_t rank, lope_comm** out) {
   if (!out) return lope_set_error(108, "null argument");
   if (nranks < 1 || rank < 0 || rank >= nranks)

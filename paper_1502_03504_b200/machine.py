@@ -22,6 +22,14 @@ Usage mirrors the reference exactly::
     m = Machine(check_program(program), RunConfig(images=4, grid_rows=2), field)
     m.run(); out = m.gather()
 
+Images are spread over the node's GPUs the way the reference spreads them over
+its images (runtime.py:97-131): image k's blocks (and device mirrors) live on GPU
+``devices[(k - 1) % len(devices)]`` (default: every visible GPU; ``devices=`` or
+``LOPE_MACHINE_DEVICES=0,1,...`` override it, repeats allowed so the mapping can be
+forced on one GPU).  A launch runs on its image's GPU; a halo slab between images on
+different GPUs is one ``lope_copy_box`` on the destination GPU reading the source
+through peer access, ordered by CUDA events between the GPUs' streams.
+
 ``dtype="float64"`` (default) reproduces the reference bit for bit; ``"float32"``
 runs the fp32 restatement.  The per-element orders
 (``RunConfig.order``) evaluate the same per-point expression, so they give the
@@ -31,6 +39,7 @@ same bits on the GPU; the launch is order-independent by construction.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -69,31 +78,51 @@ def _make_machine_class():
     class GpuMachine(lrt.Machine):
         """``lopec.runtime.Machine`` with launches and halo exchanges on the GPU."""
 
-        def __init__(self, check, config, input_field=None, dtype="float64"):
+        def __init__(self, check, config, input_field=None, dtype="float64", devices=None):
             super().__init__(check, config, input_field)
+            torch = R._torch()
             self.dtype = dtype
             self._np_dtype = np.float64 if dtype in ("float64", "f64") else np.float32
-            self._gk = {name: R.CompiledKernel(from_lopec(kir), dtype) for name, kir in self.kernels.items()}
+            if devices is None:
+                env = os.environ.get("LOPE_MACHINE_DEVICES")
+                devices = ([int(x) for x in env.split(",") if x.strip()] if env
+                           else list(range(torch.cuda.device_count())))
+            self.devices = [int(d) for d in devices] or [torch.cuda.current_device()]
+            self._gk = {}
+            for name, kir in self.kernels.items():
+                self._gk[name] = R.CompiledKernel(from_lopec(kir), dtype)
+            for a in set(self.devices):
+                with torch.cuda.device(a):
+                    for b in set(self.devices):
+                        if a != b:
+                            _lib.check(_lib.lib().lope_peer_enable(b), "lope_peer_enable")
             self._twins = {}
+
+        def device_of(self, k):
+            """GPU of image k (1-based): images round-robin over the devices."""
+            return self.devices[(k - 1) % len(self.devices)]
 
         # -- twins -----------------------------------------------------------
 
-        def _twin(self, arr, host):
+        def _twin(self, arr, host, k):
+            torch = R._torch()
             key = id(host)
             t = self._twins.get(key)
             if t is None or t.host is not host:
                 lay = arr.layout
-                dev = R.HaloArray(lay.interior, lay.lo, lay.hi, self.dtype, name=arr.entity.name)
+                with torch.cuda.device(self.device_of(k)):
+                    dev = R.HaloArray(lay.interior, lay.lo, lay.hi, self.dtype, name=arr.entity.name)
                 t = _Twin(host, dev)
                 self._twins[key] = t
             if t.state == "host":
                 src = np.ascontiguousarray(host, dtype=self._np_dtype)
-                _lib.check(_lib.lib().lope_pack_padded(ctypes.byref(t.dev.layout),
-                                                       src.ctypes.data_as(ctypes.c_void_p),
-                                                       ctypes.c_void_p(t.dev.data.data_ptr()),
-                                                       ctypes.c_void_p(R._stream_handle())),
-                           "lope_pack_padded")
-                R._torch().cuda.current_stream().synchronize()
+                with torch.cuda.device(t.dev.device):
+                    _lib.check(_lib.lib().lope_pack_padded(ctypes.byref(t.dev.layout),
+                                                           src.ctypes.data_as(ctypes.c_void_p),
+                                                           ctypes.c_void_p(t.dev.data.data_ptr()),
+                                                           ctypes.c_void_p(R._stream_handle())),
+                               "lope_pack_padded")
+                    torch.cuda.current_stream().synchronize()
                 t.state = "both"
             return t
 
@@ -103,14 +132,32 @@ def _make_machine_class():
             pend = [t for t in self._twins.values() if t.state == "device"]
             for t in pend:
                 buf = np.empty(t.host.shape, dtype=self._np_dtype)
-                _lib.check(_lib.lib().lope_unpack_padded(ctypes.byref(t.dev.layout),
-                                                         ctypes.c_void_p(t.dev.data.data_ptr()),
-                                                         buf.ctypes.data_as(ctypes.c_void_p),
-                                                         ctypes.c_void_p(R._stream_handle())),
-                           "lope_unpack_padded")
-                torch.cuda.current_stream().synchronize()
+                with torch.cuda.device(t.dev.device):
+                    _lib.check(_lib.lib().lope_unpack_padded(ctypes.byref(t.dev.layout),
+                                                             ctypes.c_void_p(t.dev.data.data_ptr()),
+                                                             buf.ctypes.data_as(ctypes.c_void_p),
+                                                             ctypes.c_void_p(R._stream_handle())),
+                               "lope_unpack_padded")
+                    torch.cuda.current_stream().synchronize()
                 t.host[:] = buf
                 t.state = "both"
+
+        def _fence(self):
+            """Order every used GPU's current stream after every other's (the BSP barrier
+            between exchange phases when images sit on several GPUs)."""
+            torch = R._torch()
+            devs = sorted(set(self.devices))
+            if len(devs) < 2:
+                return
+            evs = []
+            for d in devs:
+                e = torch.cuda.Event()
+                e.record(torch.cuda.current_stream(d))
+                evs.append(e)
+            for d in devs:
+                s = torch.cuda.current_stream(d)
+                for e in evs:
+                    s.wait_event(e)
 
         def _host_changed(self):
             """The reference code may have written any numpy block: device copies are stale."""
@@ -199,8 +246,9 @@ def _make_machine_class():
             self.events.append(("launch", k, a.kernel, on_device))
             if any(lo > hi for lo, hi in ranges):
                 return
-            twins = [self._twin(arr, host) for arr, host in bound]
-            R.launch(gk, [t.dev for t in twins], ranges, scalars)
+            twins = [self._twin(arr, host, k) for arr, host in bound]
+            with R._torch().cuda.device(self.device_of(k)):
+                R.launch(gk, [t.dev for t in twins], ranges, scalars)
             stored = set(kir.stored_arrays)
             for (p, t) in zip([q for q in gk.ir.array_params], twins):
                 if p in stored:
@@ -217,8 +265,10 @@ def _make_machine_class():
             self.events.append(("halo_transfer", name))
             rank = lay.rank
             padded = lay.padded()
-            blocks = {k: self._twin(arr, arr.blocks[k]) for k in self.images}
-            mirrors = {k: self._twin(arr, arr.mirrors[k]) for k in self.images if k in arr.mirrors}
+            blocks = {k: self._twin(arr, arr.blocks[k], k) for k in self.images}
+            mirrors = {k: self._twin(arr, arr.mirrors[k], k) for k in self.images if k in arr.mirrors}
+            torch = R._torch()
+            self._fence()
             for d in range(rank):
                 w_lo, w_hi = lay.lo[d], lay.hi[d]
                 if w_lo == 0 and w_hi == 0:
@@ -233,13 +283,16 @@ def _make_machine_class():
                     return lo3, ext
 
                 def copy(dst, src, dstart, sstart, width):
+                    # on the destination's GPU; a source on another GPU is read over
+                    # NVLink (peer access enabled at construction)
                     dlo, ext = box(dstart, width)
                     slo, _ = box(sstart, width)
-                    _lib.check(_lib.lib().lope_copy_box(
-                        ctypes.byref(dst.dev.layout), ctypes.c_void_p(dst.dev.data.data_ptr()),
-                        ctypes.c_void_p(src.dev.data.data_ptr()), (ctypes.c_int64 * 3)(*dlo),
-                        (ctypes.c_int64 * 3)(*slo), (ctypes.c_int64 * 3)(*ext),
-                        ctypes.c_void_p(R._stream_handle())), "lope_copy_box")
+                    with torch.cuda.device(dst.dev.device):
+                        _lib.check(_lib.lib().lope_copy_box(
+                            ctypes.byref(dst.dev.layout), ctypes.c_void_p(dst.dev.data.data_ptr()),
+                            ctypes.c_void_p(src.dev.data.data_ptr()), (ctypes.c_int64 * 3)(*dlo),
+                            (ctypes.c_int64 * 3)(*slo), (ctypes.c_int64 * 3)(*ext),
+                            ctypes.c_void_p(R._stream_handle())), "lope_copy_box")
 
                 low_halo, high_halo = 0, w_lo + m_d
                 low_int, high_int = w_lo, m_d
@@ -256,6 +309,7 @@ def _make_machine_class():
                         self.counters[k]["d2h"] += 1
                         self.events.append(("d2h", k, name, d))
                     blocks[k].state = "device"
+                self._fence()
                 # phase 2: neighbour fills (interior slabs are never written here, so
                 # the image order does not matter)
                 for k in self.images:
@@ -268,6 +322,7 @@ def _make_machine_class():
                         copy(blocks[k], blocks[nb], high_halo, low_int, w_hi)
                         self.events.append(("halo_fill", k, name, d, "high"))
                     blocks[k].state = "device"
+                self._fence()
                 # phase 3: push the received halo slabs down to the mirrors
                 for k in self.images:
                     if k not in mirrors:
@@ -281,6 +336,7 @@ def _make_machine_class():
                         self.counters[k]["h2d"] += 1
                         self.events.append(("h2d", k, name, d))
                     mirrors[k].state = "device"
+                self._fence()
 
     return GpuMachine
 
@@ -288,12 +344,12 @@ def _make_machine_class():
 _CLS = None
 
 
-def Machine(check, config, input_field=None, dtype="float64"):
+def Machine(check, config, input_field=None, dtype="float64", devices=None):
     """Construct the GPU-backed drop-in for ``lopec.runtime.Machine``."""
     global _CLS
     if _CLS is None:
         _CLS = _make_machine_class()
-    return _CLS(check, config, input_field, dtype)
+    return _CLS(check, config, input_field, dtype, devices)
 
 
 def machine_class():

@@ -37,12 +37,27 @@ def compile_text(text):
     return result
 
 
+def _device_maps():
+    """One GPU per image (as many as the node has), and the mapping forced onto the
+    first GPU twice (images alternate between two 'devices': the cross-device code
+    path -- per-device launches, events between streams, destination-side copies --
+    runs even on a one-GPU box)."""
+    n = torch.cuda.device_count()
+    maps = [None, [0, 0]]
+    if n > 1:
+        maps.append(list(range(n)))
+    return maps
+
+
+@pytest.mark.parametrize("devices", _device_maps(), ids=lambda d: "auto" if d is None else "dev" + "".join(map(str, d)))
 @pytest.mark.parametrize("case", CASES, ids=[c["tag"] for c in CASES])
-def test_gpu_machine_reproduces_reference_machine(case):
+def test_gpu_machine_reproduces_reference_machine(case, devices):
     result = compile_text(case["text"])
     field = ARR[case["tag"] + "_in"]
     m = Machine(result, RunConfig(images=case["images"], grid_rows=case["grid_rows"],
-                                  devices=case["devices"], steps=case["steps"]), field.copy())
+                                  devices=case["devices"], steps=case["steps"]), field.copy(), devices=devices)
+    if devices is not None:
+        assert [m.device_of(k) for k in m.images] == [devices[(k - 1) % len(devices)] for k in m.images]
     m.run()
     assert np.array_equal(m.gather(), ARR[case["tag"] + "_out"])
     for k in m.images:
