@@ -99,6 +99,15 @@ int lope_launch(const lope_kernel* k, const lope_layout* layouts, const int64_t*
 int lope_step(const lope_kernel* k, const lope_layout* layout, const void* in, void* out,
               const double* rscal, const int64_t* iscal, int32_t wrap_mask, void* stream);
 
+/* lope_step for kernels over several array parameters (runtime.py:541-618 followed by the
+ * HALO_TRANSFER of every stored array, runtime.py:643-697): one full-interior launch
+ * whose stored arrays (out[a] != in[a]) also receive their periodic images along
+ * wrap_mask dims.  Arrays the kernel never stores are read from in[a] (out[a] may be
+ * NULL) and keep their halos.  Precondition: every in[a]'s halos are valid. */
+int lope_step_arrays(const lope_kernel* k, const lope_layout* layouts, const void* const* in,
+                     void* const* out, const double* rscal, const int64_t* iscal, int32_t wrap_mask,
+                     void* stream);
+
 /* lope_step restricted to interior planes [begin, end) of the slowest dimension (0-based,
  * half-open): the slab-decomposed pipeline computes boundary planes first, exchanges
  * them, and computes the interior planes meanwhile.  Images are refreshed only along

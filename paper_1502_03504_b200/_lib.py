@@ -21,7 +21,7 @@ DTYPES = {"f32": F32, "float32": F32, "f64": F64, "float64": F64}
 
 EXPORTS = ("lope_abi_version", "lope_last_error", "lope_set_cache_dir", "lope_layout_init",
            "lope_kernel_compile", "lope_kernel_destroy", "lope_kernel_describe",
-           "lope_kernel_source", "lope_launch", "lope_step", "lope_step_planes", "lope_halo_fill", "lope_pack",
+           "lope_kernel_source", "lope_launch", "lope_step", "lope_step_arrays", "lope_step_planes", "lope_halo_fill", "lope_pack",
            "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_plan_set_variant", "lope_kernel_prepare", "lope_step_multi",
            "lope_step_planes_peer", "lope_ipc_export", "lope_ipc_open", "lope_ipc_close", "lope_copy_bytes",
            "lope_box_unpack", "lope_fill_hash", "lope_face_span", "lope_launch_count",
@@ -68,6 +68,7 @@ def lib():
     L.lope_kernel_source.argtypes = [VP, ctypes.c_char_p, SZ]
     L.lope_launch.argtypes = [VP, P(Layout), P(I64), P(VP), P(VP), P(ctypes.c_double), P(I64), VP]
     L.lope_step.argtypes = [VP, P(Layout), VP, VP, P(ctypes.c_double), P(I64), I32, VP]
+    L.lope_step_arrays.argtypes = [VP, P(Layout), P(VP), P(VP), P(ctypes.c_double), P(I64), I32, VP]
     L.lope_step_planes.argtypes = [VP, P(Layout), VP, VP, I64, I64, P(ctypes.c_double), P(I64), I32, VP]
     L.lope_halo_fill.argtypes = [P(Layout), VP, I32, VP]
     L.lope_pack.argtypes = [P(Layout), VP, VP, VP]

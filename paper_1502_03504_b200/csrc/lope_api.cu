@@ -314,6 +314,7 @@ struct TileCfg {
 struct DevMod {
   CUmodule mod = nullptr;
   CUfunction generic = nullptr;
+  CUfunction row = nullptr;             // rank-1 vector kernel
   CUfunction tiled = nullptr;
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
   int tiled_local = 0;                  // local memory (spills) per thread of the tiled kernel
@@ -329,7 +330,7 @@ template <class T> struct HArr { const T* in; T* out; long long s1, s2, org; };
 template <class T> struct HScal { T v[LOPE_HOST_MAX_SCAL]; };
 struct HGeom {
   int ext[3], m[3], r0[3], lo[3], hi[3];
-  int wrap, zchunk, xshift, box0, p1, yband;
+  int wrap, zchunk, xshift, box0, p1, yband, xexact;
   long long sdl, sdh;
 };
 
@@ -358,6 +359,8 @@ struct lope_kernel {
   std::vector<LopeVariant> variants;        // [0] = the default pick_tile() variant
   std::map<std::string, LopePlan> plans;    // geometry key -> tuned plan
   std::string describe_path;
+  // launches per kernel family (describe "launches"): which path a geometry actually took
+  mutable std::atomic<long long> n_tiled{0}, n_multi{0}, n_generic{0}, n_tblock{0}, n_row{0};
   // the default variant's fields, kept for describe/source
   const TileCfg& tile() const { return variants[0].tile; }
   bool tiled_ok() const { return variants[0].tiled_ok; }
@@ -476,6 +479,12 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
        "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
        "  lope_generic_impl<LopeBody, LT>(pack.a, sc, g);\n"
        "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
+  if (k.rank == 1) {
+    s << "extern \"C\" __global__ void __launch_bounds__(256) lope_row("
+         "const __grid_constant__ LopeArrPack pack, const LopeScal<LT> sc, const LopeGeom g) {\n"
+         "  lope_row_impl<LopeBody, LT, " << k.arrays.size() << ">(pack.a, sc, g);\n"
+         "  if (g.sdl | g.sdh) __threadfence_system();\n}\n";
+  }
   if (V.tiled_ok) {
     const TileCfg& c = V.tile;
     s << "typedef LopeTiledCfg<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
@@ -620,6 +629,10 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleLoadData");
   r = d.moduleGetFunction(&m.generic, m.mod, "lope_generic");
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_generic)");
+  if (K->ir.rank == 1) {
+    r = d.moduleGetFunction(&m.row, m.mod, "lope_row");
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_row)");
+  }
   if (V.tiled_ok) {
     r = d.moduleGetFunction(&m.tiled, m.mod, "lope_tiled");
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction(lope_tiled)");
@@ -881,27 +894,35 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   g.sdh = sdh;
   if (const char* e = std::getenv("LOPE_YBAND")) g.yband = std::atoi(e);
   const int vx = 16 / (int)sizeof(T);
-  {
-    const int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
-    g.xshift = 0;
-    g.box0 = (int)(layouts[0].base + layouts[0].lo[0] + r0[0] - padx);
-    g.p1 = tmap_flat() ? (int)layouts[0].padded[1] : 0;
-  }
+  // The tiled kernels run x from the range start rounded down to a whole 16-byte
+  // vector (interior rows start 64-byte aligned, lope_layout_init): the xsh cells in
+  // front of the range and the ragged end are masked in the stores.
+  const int xsh = r0[0] % vx;
+  const int r0x = r0[0] - xsh;
+  g.p1 = tmap_flat() ? (int)layouts[0].padded[1] : 0;
   Drv& d = drv();
-  // the vector path needs 16-byte aligned x extents; when it refreshes halo images
-  // every halo cell must have exactly one image (interior at least two lines wide in
-  // x, at least lo+hi in y and z); other geometries run on the generic kernel
-  bool geom_ok = (r0[0] % vx) == 0 && (ext[0] % vx) == 0;
+  // When the launch refreshes halo images every halo cell must have exactly one image
+  // (interior at least lo+hi wide in every wrapped dim).  x images are
+  // whole 64-byte atoms when the interior is a whole number of vectors and at least
+  // two atoms wide, else cell by cell; other geometries run on the generic kernel.
+  bool geom_ok = true;
   if (wrap) {
     const lope_layout& L0 = layouts[0];
     const long long line = 64 / (long long)sizeof(T);
-    geom_ok = geom_ok && L0.interior[0] % vx == 0 && L0.interior[0] >= 2 * line;
-    for (int d = 1; d < 3; ++d)
+    g.xexact = (wrap & 1) && !(L0.interior[0] % vx == 0 && L0.interior[0] >= 2 * line);
+    for (int d = 0; d < 3; ++d)
       if ((wrap >> d) & 1) geom_ok = geom_ok && L0.interior[d] >= L0.lo[d] + L0.hi[d];
+  }
+  if (geom_ok) {
+    // shift the x range for the tiled kernels (restored below for the generic kernel)
+    g.r0[0] = r0x;
+    g.ext[0] = ext[0] + xsh;
+    g.xshift = xsh;
   }
   const bool use_tiled = V.tiled_ok && k.arrays.size() == 1 && geom_ok &&
                          !std::getenv("LOPE_FORCE_GENERIC");
   if (use_tiled) {
+    g.box0 = (int)(layouts[0].base + layouts[0].lo[0] + r0x - ((k.fn[0][0] + vx - 1) / vx) * vx);
     const lope_layout* L = &layouts[0];
     CUtensorMap map;
     if (int e = encode_tmap(L, in[0], *m, &map)) return e;
@@ -910,10 +931,10 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     a.out = (T*)out[0];
     a.s1 = L->stride[1];
     a.s2 = L->stride[2];
-    a.org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+    a.org = L->base + (L->lo[0] + r0x) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
             (long long)(L->lo[2] + r0[2]) * L->stride[2];
     const TileCfg& c = V.tile;
-    long long ntx = (ext[0] + 32 * vx * c.bxw - 1) / (32 * vx * c.bxw);
+    long long ntx = (g.ext[0] + 32 * vx * c.bxw - 1) / (32 * vx * c.bxw);
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     long long units = ntx * nty * nzc;
@@ -964,6 +985,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     }
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tiled)");
     g_launches++;
+    K->n_tiled++;
     return 0;
   }
   // several arrays with one layout: the multi-array tiled kernel
@@ -979,7 +1001,6 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   }
   for (int a = 0; same && a < na; ++a) same = in[a] != nullptr;
   for (size_t q = 0; same && q < k.stored.size(); ++q) same = out && out[k.stored[q]] != nullptr;
-  same = same && wrap == 0;      // the multi-array kernel stores no periodic images
   if (same) {
     const lope_layout* L = &layouts[0];
     std::vector<CUtensorMap> maps(na);
@@ -992,14 +1013,14 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
       pk[a].out = out ? (T*)out[a] : nullptr;
       pk[a].s1 = L->stride[1];
       pk[a].s2 = L->stride[2];
-      pk[a].org = L->base + (L->lo[0] + r0[0]) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
+      pk[a].org = L->base + (L->lo[0] + r0x) + (long long)(L->lo[1] + r0[1]) * L->stride[1] +
                   (long long)(L->lo[2] + r0[2]) * L->stride[2];
       un0 = std::max(un0, k.fn[a][0]);
     }
     const int padx = ((un0 + vx - 1) / vx) * vx;
-    g.box0 = (int)(L->base + L->lo[0] + r0[0] - padx);
+    g.box0 = (int)(L->base + L->lo[0] + r0x - padx);
     const int ry = k.rank == 3 ? 1 : 2;
-    long long ntx = (ext[0] + 32 * vx - 1) / (32 * vx);
+    long long ntx = (g.ext[0] + 32 * vx - 1) / (32 * vx);
     long long nty = (ext[1] + 16 * ry - 1) / (16 * ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     long long units = ntx * nty * nzc;
@@ -1020,8 +1041,33 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     CUresult r = launch_ex(m->tiledm, (unsigned)grid, (unsigned)m->tm_threads, m->tm_smem, st, args);
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tiled_multi)");
     g_launches++;
+    K->n_multi++;
     return 0;
   }
+  if (k.rank == 1 && m->row && geom_ok && !std::getenv("LOPE_FORCE_GENERIC")) {
+    // rank 1: one 16-byte vector per thread, the x range rounded down to whole vectors
+    std::vector<HArr<T>> pk(k.arrays.size());
+    for (size_t i = 0; i < k.arrays.size(); ++i) {
+      pk[i].in = (const T*)in[i];
+      pk[i].out = out ? (T*)out[i] : nullptr;
+      pk[i].s1 = layouts[i].stride[1];
+      pk[i].s2 = layouts[i].stride[2];
+      pk[i].org = layouts[i].base + layouts[i].lo[0] + r0x;
+    }
+    g.xexact = 1;
+    const long long nvec = (g.ext[0] + vx - 1) / vx;
+    long long grid = std::min<long long>((nvec + 255) / 256, (long long)sm_count() * 8);
+    if (grid < 1) grid = 1;
+    void* args[] = {pk.data(), &sc, &g};
+    CUresult r = launch_ex(m->row, (unsigned)grid, 256, 0, st, args);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_row)");
+    g_launches++;
+    K->n_row++;
+    return 0;
+  }
+  g.r0[0] = r0[0];
+  g.ext[0] = ext[0];
+  g.xshift = 0;
   std::vector<HArr<T>> pack(k.arrays.size());
   for (size_t i = 0; i < k.arrays.size(); ++i) {
     const lope_layout* L = &layouts[i];
@@ -1044,6 +1090,7 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   CUresult r = d.launchKernel(m->generic, gx, gy, gz, 128, 1, 1, 0, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_generic)");
   g_launches++;
+  K->n_generic++;
   return 0;
 }
 
@@ -1153,7 +1200,7 @@ int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kerne
   if (!err.empty()) return fail(104, "kernel IR rejected: %s", err.c_str());
   K->dtype = dtype;
   if (int e = add_variant(K.get(), pick_tile(K->ir, dtype))) return e;
-  K->describe_path = K->tiled_ok() ? "tiled_tma"
+  K->describe_path = K->ir.rank == 1 ? "row" : K->tiled_ok() ? "tiled_tma"
                      : (K->variants[0].source.find("lope_tiled_multi(") != std::string::npos ? "tiled_tma_multi"
                                                                                            : "generic");
   *out = K.release();
@@ -1200,7 +1247,9 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
       << "}";
     first = false;
   }
-  o << "}}";
+  o << "},\"launches\":{\"tiled\":" << k->n_tiled.load() << ",\"tiled_multi\":" << k->n_multi.load()
+    << ",\"row\":" << k->n_row.load() << ",\"tblock\":" << k->n_tblock.load() << ",\"generic\":"
+    << k->n_generic.load() << "}}";
   std::string s = o.str();
   if (s.size() + 1 > n) return fail(108, "buffer too small (%zu needed)", s.size() + 1);
   std::memcpy(buf, s.c_str(), s.size() + 1);
@@ -1277,6 +1326,45 @@ int lope_launch(const lope_kernel* kc, const lope_layout* layouts, const int64_t
     if (e) return e;
   }
   return 0;
+}
+
+int lope_step_arrays(const lope_kernel* kc, const lope_layout* layouts, const void* const* in,
+                     void* const* out, const double* rscal, const int64_t* iscal, int32_t wrap_mask,
+                     void* stream) {
+  lope_kernel* k = const_cast<lope_kernel*>(kc);
+  if (!k || !layouts || !in) return fail(108, "null argument");
+  const lope::Kir& ir = k->ir;
+  const int na = (int)ir.arrays.size();
+  for (int a = 0; a < na; ++a) {
+    if (int e = check_layout(&layouts[a])) return e;
+    if (layouts[a].rank != ir.rank || layouts[a].dtype != k->dtype)
+      return fail(108, "array '%s' rank/dtype do not match kernel '%s'", ir.arrays[a].c_str(), ir.name.c_str());
+    for (int d = 0; d < 3; ++d) {
+      if (layouts[a].interior[d] != layouts[0].interior[d])
+        return fail(108, "array arguments have different interiors");
+      if (ir.fn[a][d] > layouts[a].lo[d] || ir.fp[a][d] > layouts[a].hi[d])
+        return fail(102, "kernel '%s' reads '%s' %d/%d cells out in dim %d but the halo is (%d,%d)",
+                    ir.name.c_str(), ir.arrays[a].c_str(), ir.fn[a][d], ir.fp[a][d], d + 1, layouts[a].lo[d],
+                    layouts[a].hi[d]);
+    }
+    if (!in[a]) return fail(202, "array '%s' is not allocated", ir.arrays[a].c_str());
+  }
+  const int wrap = wrap_mask & ((1 << ir.rank) - 1);
+  for (int q : ir.stored) {
+    if (!out || !out[q]) return fail(202, "stored array '%s' has no output buffer", ir.arrays[q].c_str());
+    if (out[q] == in[q]) return fail(108, "output buffer of '%s' aliases its snapshot", ir.arrays[q].c_str());
+    if (wrap)
+      if (int e = check_interior_halo(&layouts[q])) return e;
+    // the fused images are written for the first array's halo widths
+    for (int d = 0; d < 3; ++d)
+      if (wrap && (layouts[q].lo[d] != layouts[0].lo[d] || layouts[q].hi[d] != layouts[0].hi[d]))
+        return fail(108, "stored arrays of a fused step need the halo widths of the first array");
+  }
+  int r0[3] = {0, 0, 0}, ext[3];
+  for (int d = 0; d < 3; ++d) ext[d] = (int)layouts[0].interior[d];
+  cudaStream_t st = (cudaStream_t)stream;
+  return k->dtype == LOPE_F32 ? run_body<float>(k, layouts, r0, ext, in, out, rscal, iscal, wrap, st)
+                              : run_body<double>(k, layouts, r0, ext, in, out, rscal, iscal, wrap, st);
 }
 
 int lope_step(const lope_kernel* kc, const lope_layout* layout, const void* in, void* out,
@@ -1389,6 +1477,13 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       t.wy = 8;
       t.ry = 4;
       for (int zc : {32, 64}) c.push_back({t, zc, 0});
+      // 16 warps x 4 rows (64-row tiles, 36 KB stages, 6-deep ring): the same per-point
+      // overhead with twice the warps in flight and half the y-halo re-reads
+      TileCfg t6 = base;
+      t6.ry = 4;
+      t6.ns = 6;
+      if (tiled_smem_bytes(K->ir, K->dtype, t6) <= 225 * 1024)
+        for (int zc : {32, 64}) c.push_back({t6, zc, 0});
       t.pw = 1;
       t.ns = 12;
       t.sh = 1;
@@ -1485,6 +1580,7 @@ int lope_step_multi(const lope_kernel* kc, const lope_layout* layout, void* buf0
       }
       if (r != CUDA_SUCCESS) return cu_fail(r, "cuLaunchKernel(lope_tblock)");
       g_launches++;
+      k->n_tblock++;
       nsteps -= m->tb_tt;
     } else {
       if (int e = lope_step(k, layout, bufs[live], bufs[1 - live], rscal, iscal, full, stream)) return e;

@@ -251,12 +251,12 @@ struct Emitter {
     const Node& n = k.nodes[i];
     switch (n.kind) {
       case Node::CONST:
-        return "T(" + hexlit(n.value) + ")";
+        return "AR::c(T(" + hexlit(n.value) + "))";
       case Node::SCALAR: {
         auto it = loc_ix.find(n.name);
         if (it != loc_ix.end() && assigned.count(n.name)) return "l" + std::to_string(it->second);
         auto jt = scal_ix.find(n.name);
-        return "sc[" + std::to_string(jt->second) + "]";
+        return "AR::c(sc[" + std::to_string(jt->second) + "])";
       }
       case Node::READ: {
         bool centre = n.off[0] == 0 && n.off[1] == 0 && n.off[2] == 0;
@@ -264,8 +264,14 @@ struct Emitter {
         return "rd.template at<" + std::to_string(n.arr) + "," + std::to_string(n.off[0]) + "," +
                std::to_string(n.off[1]) + "," + std::to_string(n.off[2]) + ">()";
       }
-      case Node::ADD: return "A_::add(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
-      case Node::MUL: return "A_::mul(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      case Node::ADD: return "AR::add(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      case Node::MUL: {
+        // a product with a power-of-two constant is exact unless it underflows, and ptxas
+        // then fuses a paired multiply into the following paired add (FFMA2), which
+        // rounds differently in the subnormal range: AR::mulx keeps it a separate multiply
+        const bool p2 = pow2_const(n.kids[0]) || pow2_const(n.kids[1]);
+        return std::string(p2 ? "AR::mulx(" : "AR::mul(") + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      }
       case Node::DIV: {
         // x / 2^k == x * 2^-k exactly in IEEE arithmetic (same real value, one rounding),
         // so a power-of-two constant divisor becomes a multiply (float and double alike)
@@ -274,7 +280,7 @@ struct Emitter {
           int e = 0;
           double fr = std::frexp(d.value, &e);
           if ((fr == 0.5 || fr == -0.5) && e > -100 && e < 100)
-            return "A_::mul(" + ex(n.kids[0]) + ", T(" + hexlit(1.0 / d.value) + "))";
+            return "AR::mulx(" + ex(n.kids[0]) + ", AR::c(T(" + hexlit(1.0 / d.value) + ")))";
           // any other constant: reciprocal + FMA correction (LopeAr::divc), with the
           // correctly rounded reciprocal of the divisor as converted to each type
           const float bf = (float)d.value;
@@ -285,30 +291,37 @@ struct Emitter {
           const bool okf = std::isfinite(bf) && abf >= 0x1p-16f && abf <= 0x1p+16f && std::isfinite(yf);
           const bool okd = abd >= 0x1p-60 && abd <= 0x1p+60;
           has_divc = true;
-          return "A_::template divc<FAST>(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ", " + hexlit(yf) + ", " +
+          return "AR::template divc<FAST>(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ", " + hexlit(yf) + ", " +
                  hexlit(yd) + ", " + (okf ? "true" : "false") + ", " + (okd ? "true" : "false") + ", slow)";
         }
         if (d.kind == Node::SCALAR && !loc_ix.count(d.name) && 2 * k.scalars.size() <= 16) {
           // kernel scalar divisor: the host passes RN(1/b) (or NaN) after the scalars
           has_divc = true;
           const int i = scal_ix.at(d.name);
-          return "A_::template divs<FAST>(" + ex(n.kids[0]) + ", sc[" + std::to_string(i) + "], sc[" +
+          return "AR::template divs<FAST>(" + ex(n.kids[0]) + ", sc[" + std::to_string(i) + "], sc[" +
                  std::to_string(k.scalars.size() + i) + "], slow)";
         }
-        return "A_::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+        return "AR::div(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
       }
-      case Node::NEG: return "A_::neg(" + ex(n.kids[0]) + ")";
-      case Node::ABS: return "A_::abs_(" + ex(n.kids[0]) + ")";
-      case Node::SQRT: return "A_::sqrt_(" + ex(n.kids[0]) + ")";
+      case Node::NEG: return "AR::neg(" + ex(n.kids[0]) + ")";
+      case Node::ABS: return "AR::abs_(" + ex(n.kids[0]) + ")";
+      case Node::SQRT: return "AR::sqrt_(" + ex(n.kids[0]) + ")";
       case Node::MIN:
       case Node::MAX: {
-        const char* f = n.kind == Node::MIN ? "lope_min<T>" : "lope_max<T>";
+        const char* f = n.kind == Node::MIN ? "AR::min_" : "AR::max_";
         std::string acc = ex(n.kids[0]);
         for (size_t q = 1; q < n.kids.size(); ++q) acc = std::string(f) + "(" + acc + ", " + ex(n.kids[q]) + ")";
         return acc;
       }
     }
-    return "T(0)";
+    return "AR::c(T(0))";
+  }
+  bool pow2_const(int i) const {
+    const Node& c = k.nodes[i];
+    if (c.kind != Node::CONST || c.value == 0.0 || !std::isfinite(c.value)) return false;
+    int e = 0;
+    const double fr = std::frexp(c.value, &e);
+    return fr == 0.5 || fr == -0.5;
   }
   std::set<std::string> assigned;   // locals assigned so far
   bool has_divc = false;            // a constant division went through LopeAr::divc
@@ -364,13 +377,14 @@ std::string emit_body(const Kir& k) {
     }
   }
   o << "  static constexpr bool HAS_DIVC = " << (E.has_divc ? "true" : "false") << ";\n";
-  o << "  template <class T, bool FAST, class RD>\n";
-  o << "  static __device__ __forceinline__ void eval(const RD& rd, const T* __restrict__ sc, T* res, bool& slow) {\n";
-  o << "    typedef LopeAr<T> A_;\n";
+  // W = T (one point) or a pair type evaluating two points per instruction (LopeAr2:
+  // FADD2 / FMUL2 on sm_100, same IEEE round-to-nearest per element)
+  o << "  template <class T, bool FAST, class RD, class W = T, class AR = LopeAr<T>>\n";
+  o << "  static __device__ __forceinline__ void eval(const RD& rd, const T* __restrict__ sc, W* res, bool& slow) {\n";
   o << "    (void)sc;\n";
   o << "    (void)slow;\n";
-  for (size_t i = 0; i < k.locals.size(); ++i) o << "    T l" << i << " = T(0);\n";
-  for (int a : k.stored) o << "    T p" << a << " = T(0);\n";
+  for (size_t i = 0; i < k.locals.size(); ++i) o << "    W l" << i << " = AR::c(T(0));\n";
+  for (int a : k.stored) o << "    W p" << a << " = AR::c(T(0));\n";
   o << b.str();
   for (size_t q = 0; q < k.stored.size(); ++q) o << "    res[" << q << "] = p" << k.stored[q] << ";\n";
   o << "  }\n};\n";

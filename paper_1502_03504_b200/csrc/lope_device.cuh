@@ -32,9 +32,15 @@ typedef unsigned int lope_u32;
 // IEEE arithmetic (per-node rounding, numpy NaN semantics for min/max)
 
 template <class T> struct LopeAr;
+template <class T> __device__ __forceinline__ T lope_min(T a, T b);
+template <class T> __device__ __forceinline__ T lope_max(T a, T b);
 template <> struct LopeAr<float> {
+  static __device__ __forceinline__ float c(float a) { return a; }
+  static __device__ __forceinline__ float min_(float a, float b) { return lope_min<float>(a, b); }
+  static __device__ __forceinline__ float max_(float a, float b) { return lope_max<float>(a, b); }
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float mulx(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
   static __device__ __forceinline__ float neg(float a) { return -a; }
   static __device__ __forceinline__ float abs_(float a) { return fabsf(a); }
@@ -89,8 +95,12 @@ template <> struct LopeAr<float> {
   }
 };
 template <> struct LopeAr<double> {
+  static __device__ __forceinline__ double c(double a) { return a; }
+  static __device__ __forceinline__ double min_(double a, double b) { return lope_min<double>(a, b); }
+  static __device__ __forceinline__ double max_(double a, double b) { return lope_max<double>(a, b); }
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double mulx(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
   static __device__ __forceinline__ double neg(double a) { return -a; }
   static __device__ __forceinline__ double abs_(double a) { return fabs(a); }
@@ -162,6 +172,43 @@ template <> struct LopeAr<double> {
 template <class T> __device__ __forceinline__ T lope_min(T a, T b) { return (a != a || a < b) ? a : b; }
 template <class T> __device__ __forceinline__ T lope_max(T a, T b) { return (a != a || a > b) ? a : b; }
 
+// Two fp32 points per instruction (sm_100 FADD2 / FMUL2: two IEEE round-to-nearest
+// results, subnormals kept -- the same bits as two FADD / FMUL).  Operations without
+// a paired form run element by element through LopeAr<float>.
+struct LopeAr2 {
+  typedef float2 W;
+  typedef LopeAr<float> S;
+  static __device__ __forceinline__ W c(float a) { return make_float2(a, a); }
+  // PTX add.rn.f32x2 (FADD2)
+  static __device__ __forceinline__ W add(W a, W b) {
+    W d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+  }
+  // Products stay scalar (two FMUL): ptxas contracts a paired multiply feeding a paired
+  // add into FFMA2 even with an explicit .rn, which would change the rounding.
+  static __device__ __forceinline__ W mul(W a, W b) { return make_float2(S::mul(a.x, b.x), S::mul(a.y, b.y)); }
+  // an exact-looking product (power-of-two constant) as two scalar multiplies
+  static __device__ __forceinline__ W mulx(W a, W b) { return make_float2(S::mul(a.x, b.x), S::mul(a.y, b.y)); }
+  static __device__ __forceinline__ W div(W a, W b) { return make_float2(S::div(a.x, b.x), S::div(a.y, b.y)); }
+  static __device__ __forceinline__ W neg(W a) { return make_float2(-a.x, -a.y); }
+  static __device__ __forceinline__ W abs_(W a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+  static __device__ __forceinline__ W sqrt_(W a) { return make_float2(S::sqrt_(a.x), S::sqrt_(a.y)); }
+  static __device__ __forceinline__ W min_(W a, W b) { return make_float2(lope_min(a.x, b.x), lope_min(a.y, b.y)); }
+  static __device__ __forceinline__ W max_(W a, W b) { return make_float2(lope_max(a.x, b.x), lope_max(a.y, b.y)); }
+  template <bool FAST>
+  static __device__ __forceinline__ W divs(W x, float b, float y, bool& slow) {
+    return make_float2(S::template divs<FAST>(x.x, b, y, slow), S::template divs<FAST>(x.y, b, y, slow));
+  }
+  template <bool FAST>
+  static __device__ __forceinline__ W divc(W x, W b, double yf, double yd, bool okf, bool okd, bool& slow) {
+    return make_float2(S::template divc<FAST>(x.x, b.x, yf, yd, okf, okd, slow),
+                       S::template divc<FAST>(x.y, b.x, yf, yd, okf, okd, slow));
+  }
+};
+
 // --------------------------------------------------------------------------
 // Parameters
 
@@ -187,10 +234,11 @@ struct LopeGeom {
   int lo[3], hi[3];
   int wrap;       // bit d: refresh periodic halo images along dim d in the epilogue
   int zchunk;     // tiled: planes per work unit
-  int xshift;     // tiled: elements the TMA box starts early so its start is 16-byte aligned
+  int xshift;     // tiled: leading elements of the (vector-aligned) range outside the launch range
   int box0;       // tiled: TMA x coordinate of tile 0's box (row-relative, already shifted)
   int p1;         // tiled: padded rows per plane; > 0 selects the flattened 2-D tensor map
   int yband;      // tiled: tile rows per band of the unit walk (0: whole plane)
+  int xexact;     // tiled: x images cell by cell (m[0] not a whole number of vectors / atoms)
   // Fused exchange: periodic images along the slowest dim go to another buffer --
   // the low / high neighbour's output block (NVLink peer memory under CUDA IPC) --
   // at this element offset from `out` (0: the image lives in this block's halo).
@@ -335,7 +383,11 @@ __device__ __forceinline__ void lope_mbar_wait_slow(lope_u32 addr, lope_u32 pari
 // Fast path: one non-blocking probe (the phase has usually completed -- the producer
 // runs NS-HOLD planes ahead); only a miss enters the suspending, bounded wait loop.
 __device__ __forceinline__ void lope_mbar_wait_addr(lope_u32 addr, lope_u32 parity) {
+#ifdef LOPE_NO_PROBE
+  lope_mbar_wait_slow(addr, parity);
+#else
   if (!lope_mbar_test_addr(addr, parity)) lope_mbar_wait_slow(addr, parity);
+#endif
 }
 __device__ __forceinline__ void lope_mbar_arrive_addr(lope_u32 addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
@@ -438,6 +490,176 @@ template <> struct LopeVec<float> { typedef float4 V; };
 template <> struct LopeVec<double> { typedef double2 V; };
 
 
+// --------------------------------------------------------------------------
+// One lane's 16-byte output vector and the periodic images the fused epilogue owes
+// (shared by the tiled kernels).  x runs from the launch range's start rounded down
+// to a whole vector: the first g.xshift cells and the cells past g.ext[0] are outside
+// the range (ragged starts / extents store element by element).  When images are
+// refreshed m[d] >= lo[d] + hi[d] (each halo cell has exactly one image); x images
+// are whole 64-byte atoms (padding included; the layout reserves an atom per side)
+// when m[0] is a multiple of the vector and >= 2 atoms, else cell by cell (g.xexact).
+// y and z images are whole rows / planes; slowest-dim images may live in a
+// neighbour's block (g.sdl / g.sdh: NVLink peer memory).
+
+template <class T, int RANK>
+struct LopeVecOut {
+  typedef typename LopeVec<T>::V V;
+  static constexpr int VX = 16 / (int)sizeof(T);
+  static constexpr int SEC = 64 / (int)sizeof(T);     // one 64-byte DRAM atom
+  static constexpr unsigned ALL = (1u << VX) - 1u;
+  int xg, ximg;
+  unsigned xm;       // bit e: element e lies inside the launch range
+  bool xw;
+  __device__ __forceinline__ void init(int x, bool xok, const LopeGeom& g) {
+    xg = x + g.r0[0];
+    xw = (g.wrap & 1) && xok &&
+         (g.xexact ? (xg < g.hi[0] || xg + VX > g.m[0] - g.lo[0])
+                   : ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC)));
+    ximg = xg < SEC ? g.m[0] : -g.m[0];
+    xm = 0;
+#pragma unroll
+    for (int e = 0; e < VX; ++e) xm |= (x + e >= g.xshift && x + e < g.ext[0]) ? (1u << e) : 0u;
+  }
+  // the vector itself (element stores only where it straddles an end of the range)
+  __device__ __forceinline__ void put(T* p, const V& o) const {
+    if (xm == ALL) {
+      *reinterpret_cast<V*>(p) = o;
+    } else {
+      const T* oe = reinterpret_cast<const T*>(&o);
+#pragma unroll
+      for (int e = 0; e < VX; ++e)
+        if ((xm >> e) & 1u) p[e] = oe[e];
+    }
+  }
+  // its x images (xw lanes only)
+  __device__ __forceinline__ void putx(T* p, const V& o, const LopeGeom& g) const {
+    if (!g.xexact) {
+      *reinterpret_cast<V*>(p + ximg) = o;
+    } else {
+      const T* oe = reinterpret_cast<const T*>(&o);
+#pragma unroll
+      for (int e = 0; e < VX; ++e) {
+        if (!((xm >> e) & 1u)) continue;
+        if (xg + e < g.hi[0]) p[e + g.m[0]] = oe[e];
+        if (xg + e >= g.m[0] - g.lo[0]) p[e - g.m[0]] = oe[e];
+      }
+    }
+  }
+  // the vector at p (row yg of the range, plane with z-image flag zw / offset zimg)
+  // with every image: x, y, z and their combinations
+  __device__ __forceinline__ void store_all(T* p, const V& o, int yg, bool zw, lope_i64 zimg, lope_i64 s1,
+                                            const LopeGeom& g) const {
+    put(p, o);
+    if (xw) putx(p, o, g);
+    const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
+    if (yw | zw) {
+      // y images (rank 2: the slowest dim, possibly in a neighbour's block)
+      const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdl : 0)
+                                          : -(lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdh : 0));
+      if (yw) {
+        put(p + yimg, o);
+        if (xw) putx(p + yimg, o, g);
+      }
+      if (zw) {
+        put(p + zimg, o);
+        if (xw) putx(p + zimg, o, g);
+        if (yw) {
+          put(p + zimg + yimg, o);
+          if (xw) putx(p + zimg + yimg, o, g);
+        }
+      }
+    }
+  }
+};
+
+// --------------------------------------------------------------------------
+// Rank-1 path (any number of arrays): each thread owns one 16-byte vector of every
+// array (coalesced LDG.128 through the read-only path) and reads the x halo of its
+// points with scalar loads that hit L1 (the neighbouring lanes' lines).  x runs from
+// the range start rounded down to a whole vector; cells outside the launch range are
+// computed and dropped.  Periodic images (lope_step) are stored cell by cell.
+
+template <class T, int NA, int VX> struct LopeRowReader {
+  const T* p[NA];      // this thread's first element in each array's snapshot
+  const T* vec;        // [NA][VX] the thread's vectors
+  int v;               // compile-time after unrolling
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ T at() const {
+    if (v + DX >= 0 && v + DX < VX) return vec[A * VX + v + DX];
+    return __ldg(p[A] + v + DX);
+  }
+};
+
+template <class Body, class T, int NA>
+__device__ __forceinline__ void lope_row_impl(const LopeArr<T>* arrs, const LopeScal<T>& sc, const LopeGeom& g) {
+  typedef typename LopeVec<T>::V V;
+  constexpr int VX = 16 / (int)sizeof(T);
+  const int nvec = (g.ext[0] + VX - 1) / VX;
+  // launched with programmatic dependent launch: wait for the previous kernel's writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int vi = blockIdx.x * blockDim.x + threadIdx.x; vi < nvec; vi += gridDim.x * blockDim.x) {
+    const int x = vi * VX;
+    T vec[NA][VX];
+    LopeRowReader<T, NA, VX> rd;
+    rd.vec = &vec[0][0];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      rd.p[a] = arrs[a].in + arrs[a].org + x;
+      const V vv = __ldg(reinterpret_cast<const V*>(rd.p[a]));
+      const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+      for (int e = 0; e < VX; ++e) vec[a][e] = ve[e];
+    }
+    T res[VX][Body::NSTORE > 0 ? Body::NSTORE : 1];
+    // branch-free points (FAST constant division); a flagged operand redoes them exactly
+    constexpr bool FAST = Body::HAS_DIVC;
+    bool slow = false;
+#pragma unroll
+    for (int v = 0; v < VX; ++v) {
+      rd.v = v;
+      Body::template eval<T, FAST>(rd, sc.v, res[v], slow);
+    }
+    if (FAST && slow) {
+#pragma unroll
+      for (int v = 0; v < VX; ++v) {
+        rd.v = v;
+        bool dummy = false;
+        Body::template eval<T, false>(rd, sc.v, res[v], dummy);
+      }
+    }
+    const bool xfull = x >= g.xshift && x + VX <= g.ext[0];
+    const int xg = x + g.r0[0];
+    const bool img = (g.wrap & 1) && (xg < g.hi[0] || xg + VX > g.m[0] - g.lo[0]);
+#pragma unroll
+    for (int q = 0; q < Body::NSTORE; ++q) {
+      const int A = Body::stored(q);
+      T* o = arrs[A].out + arrs[A].org + x;
+      if (xfull) {
+        V ov;
+        T* oe = reinterpret_cast<T*>(&ov);
+#pragma unroll
+        for (int e = 0; e < VX; ++e) oe[e] = res[e][q];
+        *reinterpret_cast<V*>(o) = ov;
+      } else {
+#pragma unroll
+        for (int e = 0; e < VX; ++e)
+          if (x + e >= g.xshift && x + e < g.ext[0]) o[e] = res[e][q];
+      }
+      if (img) {
+        // images of the first hi cells go to x+m (the low neighbour's block: sdl),
+        // of the last lo cells to x-m (the high neighbour's: sdh)
+#pragma unroll
+        for (int e = 0; e < VX; ++e) {
+          if (x + e < g.xshift || x + e >= g.ext[0]) continue;
+          if (xg + e < g.hi[0]) o[e + g.m[0] + g.sdl] = res[e][q];
+          if (xg + e >= g.m[0] - g.lo[0]) o[e - g.m[0] + g.sdh] = res[e][q];
+        }
+      }
+    }
+  }
+}
+
 template <class T, int NR, int NXW, int FZN, int FN0, int FN1, int RY, int VX, bool ZHIST>
 struct LopeWinReader {
   const T* win;    // [NZW][NR][NXW] register window (flattened)
@@ -449,6 +671,28 @@ struct LopeWinReader {
     return win[((DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0)];
   }
 };
+
+// The same window read as adjacent point pairs (v, v+1) for the paired fp32 evaluation.
+template <class T, int NR, int NXW, int FZN, int FN0, int FN1, int RY, int VX, bool ZHIST>
+struct LopeWinReader2 {
+  const T* win;
+  const T* hist;
+  int r, v;        // v even
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ float2 at() const {
+    if (ZHIST && DZ < 0) {
+      const int h = ((-DZ - 1) * RY + r) * VX + v;
+      return make_float2(hist[h], hist[h + 1]);
+    }
+    const int i = ((DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0);
+    return make_float2(win[i], win[i + 1]);
+  }
+};
+#ifndef LOPE_NO_PAIR
+#define LOPE_PAIR 1
+#else
+#define LOPE_PAIR 0
+#endif
 
 // Reads the staged planes in shared memory directly (the exact re-evaluation of a
 // plane whose fast evaluation flagged a slow-range division).
@@ -630,10 +874,6 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
   const int cx = (wx * 32 + lane) * VX;    // first column of this lane within the tile
   const int row0 = wy * RY;                // first row within the tile
   const lope_i64 s1 = a.s1, s2 = a.s2;
-  constexpr int SEC = 64 / (int)sizeof(T);          // one 64-byte DRAM atom
-  // The host sends only geometries with ext[0] % VX == 0 and, when images are
-  // refreshed, m[0] >= 2*SEC, m[0] % VX == 0 and m[d] >= lo[d] + hi[d] (each halo
-  // cell has exactly one image); anything else runs on the generic kernel.
   const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
 
   LopeUnitWalk w;
@@ -653,13 +893,10 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
     const int ybase = w.ty() * C::BY + row0;
     const bool xok = x < g.ext[0];
     const int nrow = min(RY, g.ext[1] - ybase);
-    // Periodic images (lope_step): x images are whole 64-byte atoms written by the
-    // lanes whose vectors land in the halo atom (padding included; the layout
-    // reserves an atom per side), y and z images are whole rows / planes.
-    const int xg = x + g.r0[0];
-    const bool xw = (g.wrap & 1) && xok && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
-    const int ximg = xg < SEC ? g.m[0] : -g.m[0];
-    const bool wx_any = __any_sync(0xffffffffu, xw);
+    // stores and periodic images (lope_step) of this lane's vector (LopeVecOut)
+    LopeVecOut<T, Body::RANK> vo;
+    vo.init(x, xok, g);
+    const bool wx_any = __any_sync(0xffffffffu, vo.xw);
     const bool wy_any = (g.wrap & 2) && (nrow > 0) &&
                         (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
                          lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
@@ -750,16 +987,32 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
         }
         const int r = q - Body::FN1 - Body::FP1;
         if (r >= 0) {
+          if (LOPE_PAIR && sizeof(T) == 4) {
+            // fp32: two points per FADD2 / FMUL2
 #pragma unroll
-          for (int v = 0; v < VX; ++v) {
-            LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
-            rd.win = &win[0][0][0];
-            rd.hist = &hist[0][0][0];
-            rd.r = r;
-            rd.v = v;
-            T res[1];
-            Body::template eval<T, FAST>(rd, sc.v, res, slow);
-            vals[r][v] = res[0];
+            for (int v = 0; v < VX; v += 2) {
+              LopeWinReader2<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+              rd.win = &win[0][0][0];
+              rd.hist = &hist[0][0][0];
+              rd.r = r;
+              rd.v = v;
+              float2 res[1];
+              Body::template eval<T, FAST, decltype(rd), float2, LopeAr2>(rd, sc.v, res, slow);
+              vals[r][v] = res[0].x;
+              vals[r][v + 1] = res[0].y;
+            }
+          } else {
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+              LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+              rd.win = &win[0][0][0];
+              rd.hist = &hist[0][0][0];
+              rd.r = r;
+              rd.v = v;
+              T res[1];
+              Body::template eval<T, FAST>(rd, sc.v, res, slow);
+              vals[r][v] = res[0];
+            }
           }
           if (ZHIST && !FAST) {
             // row r of the history only feeds row r: shift it now
@@ -838,8 +1091,8 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
           for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
-          *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
-          if (wx_any && xw) *reinterpret_cast<V*>(orow + (lope_i64)r * s1 + ximg) = o;
+          vo.put(orow + (lope_i64)r * s1, o);
+          if (wx_any && vo.xw) vo.putx(orow + (lope_i64)r * s1, o, g);
         }
       } else {
         // z images (rank 3: the slowest dim, possibly in a neighbour's block)
@@ -851,28 +1104,7 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
           T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
           for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
-          T* p = orow + (lope_i64)r * s1;
-          *reinterpret_cast<V*>(p) = o;
-          if (xw) *reinterpret_cast<V*>(p + ximg) = o;
-          const int yg = ybase + r + g.r0[1];
-          const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
-          if (yw | zw) {
-            // y images (rank 2: the slowest dim, possibly in a neighbour's block)
-            const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdl : 0)
-                                                : -(lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdh : 0));
-            if (yw) {
-              *reinterpret_cast<V*>(p + yimg) = o;
-              if (xw) *reinterpret_cast<V*>(p + yimg + ximg) = o;
-            }
-            if (zw) {
-              *reinterpret_cast<V*>(p + zimg) = o;
-              if (xw) *reinterpret_cast<V*>(p + zimg + ximg) = o;
-              if (yw) {
-                *reinterpret_cast<V*>(p + zimg + yimg) = o;
-                if (xw) *reinterpret_cast<V*>(p + zimg + yimg + ximg) = o;
-              }
-            }
-          }
+          vo.store_all(orow + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
         }
       }
     }
@@ -1024,19 +1256,36 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
       }
       T vals[RY][VX];
 #pragma unroll
-      for (int r = 0; r < RY; ++r)
+      for (int r = 0; r < RY; ++r) {
+        if (LOPE_PAIR && sizeof(T) == 4) {
 #pragma unroll
-        for (int v = 0; v < VX; ++v) {
-          LopeWinReader<T, NR, NXW, 0, FN0, FN1, RY, VX, false> rd;
-          rd.win = &win[0][0][0];
-          rd.hist = nullptr;
-          rd.r = r;
-          rd.v = v;
-          T res[1];
-          bool slow = false;
-          Body::template eval<T, false>(rd, sc.v, res, slow);
-          vals[r][v] = res[0];
+          for (int v = 0; v < VX; v += 2) {
+            LopeWinReader2<T, NR, NXW, 0, FN0, FN1, RY, VX, false> rd;
+            rd.win = &win[0][0][0];
+            rd.hist = nullptr;
+            rd.r = r;
+            rd.v = v;
+            float2 res[1];
+            bool slow = false;
+            Body::template eval<T, false, decltype(rd), float2, LopeAr2>(rd, sc.v, res, slow);
+            vals[r][v] = res[0].x;
+            vals[r][v + 1] = res[0].y;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < VX; ++v) {
+            LopeWinReader<T, NR, NXW, 0, FN0, FN1, RY, VX, false> rd;
+            rd.win = &win[0][0][0];
+            rd.hist = nullptr;
+            rd.r = r;
+            rd.v = v;
+            T res[1];
+            bool slow = false;
+            Body::template eval<T, false>(rd, sc.v, res, slow);
+            vals[r][v] = res[0];
+          }
         }
+      }
       if (!act) continue;
       if (s < TT) {
 #pragma unroll
@@ -1087,8 +1336,8 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
 // The single-array kernel's structure with one TMA box per array per plane in each
 // ring stage (one mbarrier, NA boxes of bytes), the union of the arrays' footprints as
 // the box halo, all NZW planes of a unit held in the ring (no z history) and the
-// producer in warp 0 lane 0.  Used by plain launches (lope_launch), which store the
-// interior only.
+// producer in warp 0 lane 0.  Plain launches (lope_launch) store the interior only;
+// fused steps (lope_step_arrays) also store every stored array's periodic images.
 
 template <class T, int NA, int NZW, int NR, int NXW, int FN0, int FN1, int FZN>
 struct LopeWinReaderM {
@@ -1097,6 +1346,17 @@ struct LopeWinReaderM {
   template <int A, int DX, int DY, int DZ>
   __device__ __forceinline__ T at() const {
     return win[((A * NZW + DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0)];
+  }
+};
+
+template <class T, int NA, int NZW, int NR, int NXW, int FN0, int FN1, int FZN>
+struct LopeWinReaderM2 {
+  const T* win;
+  int r, v;        // v even
+  template <int A, int DX, int DY, int DZ>
+  __device__ __forceinline__ float2 at() const {
+    const int i = ((A * NZW + DZ + FZN) * NR + (r + DY + FN1)) * NXW + (v + DX + FN0);
+    return make_float2(win[i], win[i + 1]);
   }
 };
 
@@ -1221,6 +1481,8 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
     const int x = w.tx * C::BX + cx;
     const int ybase = w.ty() * C::BY + row0;
     const bool xok = x < g.ext[0];
+    LopeVecOut<T, Body::RANK> vo;
+    vo.init(x, xok, g);
     const int nrow = min(RY, g.ext[1] - ybase);
     const lope_i64 rowoff = x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
     for (int pz = 0; pz < nz; ++pz) {
@@ -1253,18 +1515,38 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
 #pragma unroll
             for (int e = 0; e < FP0; ++e) win[a][k][q][FN0 + VX + e] = rp[VX + e];
           }
-      T vals[RY][VX][Body::NSTORE > 0 ? Body::NSTORE : 1];
+      constexpr int NSQ = Body::NSTORE > 0 ? Body::NSTORE : 1;
+      T vals[RY][VX][NSQ];
 #pragma unroll
-      for (int r = 0; r < RY; ++r)
+      for (int r = 0; r < RY; ++r) {
+        if (LOPE_PAIR && sizeof(T) == 4) {
 #pragma unroll
-        for (int v = 0; v < VX; ++v) {
-          LopeWinReaderM<T, NA, NZW, NR, NXW, FN0, FN1, FZN> rd;
-          rd.win = &win[0][0][0][0];
-          rd.r = r;
-          rd.v = v;
-          bool slow = false;
-          Body::template eval<T, false>(rd, sc.v, vals[r][v], slow);
+          for (int v = 0; v < VX; v += 2) {
+            LopeWinReaderM2<T, NA, NZW, NR, NXW, FN0, FN1, FZN> rd;
+            rd.win = &win[0][0][0][0];
+            rd.r = r;
+            rd.v = v;
+            bool slow = false;
+            float2 res[NSQ];
+            Body::template eval<T, false, decltype(rd), float2, LopeAr2>(rd, sc.v, res, slow);
+#pragma unroll
+            for (int q = 0; q < NSQ; ++q) {
+              vals[r][v][q] = res[q].x;
+              vals[r][v + 1][q] = res[q].y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < VX; ++v) {
+            LopeWinReaderM<T, NA, NZW, NR, NXW, FN0, FN1, FZN> rd;
+            rd.win = &win[0][0][0][0];
+            rd.r = r;
+            rd.v = v;
+            bool slow = false;
+            Body::template eval<T, false>(rd, sc.v, vals[r][v], slow);
+          }
         }
+      }
       __syncwarp();
       if (lane == 0) {
         lope_mbar_arrive(&empty[(lbase + pz) % NS]);
@@ -1272,8 +1554,11 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
           for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
       }
       if (!xok || nrow <= 0) continue;
-      // plain launches only (lope_launch): stored arrays get their interior points; the
-      // periodic images are refreshed by the next HALO_TRANSFER (lope_halo_fill)
+      // stored arrays get their interior points and, for a fused step (lope_step_arrays),
+      // the periodic images the next HALO_TRANSFER would write
+      const int zg = z0 + pz + g.r0[2];
+      const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
+      const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
 #pragma unroll
       for (int q = 0; q < Body::NSTORE; ++q) {
         T* ob = arrs.a[Body::stored(q)].out + arrs.a[Body::stored(q)].org + rowoff + (lope_i64)pz * s2;
@@ -1284,7 +1569,10 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
           T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
           for (int e = 0; e < VX; ++e) oe[e] = vals[r][e][q];
-          *reinterpret_cast<V*>(ob + (lope_i64)r * s1) = o;
+          if (g.wrap)
+            vo.store_all(ob + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
+          else
+            vo.put(ob + (lope_i64)r * s1, o);
         }
       }
     }

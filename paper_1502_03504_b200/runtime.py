@@ -221,6 +221,7 @@ class PlanTuner:
     WATCH = 12      # steps in the watchdog's window
     SLOW = 1.2      # watchdog threshold relative to the winner's tuned time
     SAFE_ZCHUNK = 16  # plans with at least this many planes per unit have no slow mode
+    SAFE_MARGIN = 1.05  # fall back only if the slow mode is this much slower than the safe plan
 
     def __init__(self, kernel: "CompiledKernel", layout, wrap_mask: int):
         self.kernel = kernel
@@ -245,7 +246,8 @@ class PlanTuner:
         self.monitoring = False
         self._watch = []             # (start, end) events of recent steps, oldest first
         self._durations = []
-        self._safe = None            # (candidate, tuned ms) of the best long-chunk plan
+        self._safe = None            # (long-chunk candidate, the winner's fastest step ms)
+        self._safe_ms = 0.0          # the long-chunk candidate's own tuned ms
 
     @property
     def steps_needed(self) -> int:
@@ -303,6 +305,7 @@ class PlanTuner:
         if self.cands[ci][1] < self.SAFE_ZCHUNK and safe:
             cs = min(safe, key=best.get)
             self._safe = (cs, min(acc[ci]))     # the winner's fastest trial: its fast mode
+            self._safe_ms = best[cs]            # what the long-chunk plan itself costs
             self.monitoring = True
         desc = json.loads(self.kernel.describe())
         self.report = {"candidates": [list(self.cands[c]) + [round(best[c], 5)] for c in sorted(best)],
@@ -330,7 +333,9 @@ class PlanTuner:
         if len(self._durations) == self.WATCH:
             med = sorted(self._durations)[self.WATCH // 2]
             cs, tuned_ms = self._safe
-            if med > self.SLOW * tuned_ms:
+            # switch only when the long-chunk plan is expected to be faster than the slow
+            # mode itself (on some boxes every long-chunk plan runs at slow-mode speed)
+            if med > self.SLOW * tuned_ms and med > self.SAFE_MARGIN * self._safe_ms:
                 self._set(*self.cands[cs])
                 self.monitoring = False
                 self._watch = []
@@ -511,6 +516,45 @@ def _step(kernel: CompiledKernel, arr: HaloArray, scalars=None, wrap_mask: Optio
     arr.swap()
     if tuner is not None:
         tuner.after(stream)
+
+
+def step_arrays(kernel: CompiledKernel, arrays: Sequence[HaloArray], scalars=None,
+                wrap_mask: Optional[int] = None, stream=None) -> None:
+    """``step`` for kernels over several arrays: one fused full-interior launch whose
+    stored arrays also receive their periodic images (``lope_step_arrays``) -- the state
+    after the launch and the next ``HALO_TRANSFER`` of every stored array."""
+    ir = kernel.ir
+    if len(arrays) != len(ir.array_params):
+        raise RuntimeFault(ALLOC_SHAPE, f"kernel '{ir.name}' takes {len(ir.array_params)} arrays")
+    if len({id(a) for a in arrays}) != len(arrays):
+        raise RuntimeFault(ALLOC_SHAPE, "the same array is bound to two kernel parameters")
+    mask = (1 << ir.rank) - 1 if wrap_mask is None else wrap_mask
+    na = len(arrays)
+    layouts = (_lib.Layout * na)(*[a.layout for a in arrays])
+    ins = (ctypes.c_void_p * na)(*[a.data.data_ptr() for a in arrays])
+    stored = set(ir.stored_arrays)
+    outs = (ctypes.c_void_p * na)(*[(a.spare(stream).data_ptr() if p in stored else None)
+                                    for p, a in zip(ir.array_params, arrays)])
+    rs, is_ = kernel.scalar_args(scalars)
+    with _nvtx(f"lope.step_arrays {ir.name}"):
+        _lib.check(_lib.lib().lope_step_arrays(kernel.handle, layouts, ins, outs, rs, is_, mask,
+                                               ctypes.c_void_p(_stream_handle(stream))), "lope_step_arrays")
+    for p, a in zip(ir.array_params, arrays):
+        if p in stored:
+            a.swap()
+
+
+def iterate_arrays(kernel: CompiledKernel, arrays: Sequence[HaloArray], steps: int, scalars=None,
+                   stream=None) -> None:
+    """``do it = 1, steps; HALO_TRANSFER(every array); do concurrent call K(arrays); end do``
+    for kernels over several arrays: fused steps, then a plain final launch."""
+    if steps <= 0:
+        return
+    for a in arrays:
+        halo_transfer(a, stream=stream)
+    for _ in range(steps - 1):
+        step_arrays(kernel, arrays, scalars, stream=stream)
+    launch(kernel, arrays, None, scalars, stream=stream)
 
 
 def multi_step(kernel: CompiledKernel, arr: HaloArray, nsteps: int, scalars=None, stream=None) -> None:

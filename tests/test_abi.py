@@ -73,7 +73,9 @@ def test_kernels_compile_and_describe():
         if name in ("lap3d7", "ninept2d", "box5x5", "drift2"):
             assert d["path"] == "tiled_tma"
         else:
-            assert d["path"] == "generic"
+            assert d["path"] == "row"       # rank 1: the vector row kernel
+            assert "lope_row(" in _lib.source(h)
+        assert set(d["launches"]) == {"tiled", "tiled_multi", "row", "tblock", "generic"}
         src = _lib.source(h)
         assert "__fadd_rn" in src and "cp.async.bulk.tensor" in src
         _lib.destroy_kernel(h)
@@ -153,7 +155,12 @@ def test_plan_watchdog_falls_back_only_on_the_slow_mode():
     calls = []
     t._set = lambda *c: calls.append(c)
     # fast mode 1.40 ms, power cap pushes steps to 1.52 ms: keep the plan
-    t._safe, t.monitoring, t._durations = (0, 1.40), True, [1.52] * PlanTuner.WATCH
+    t._safe, t._safe_ms, t.monitoring, t._durations = (0, 1.40), 1.62, True, [1.52] * PlanTuner.WATCH
+    t._check_window()
+    assert t.monitoring and not calls and t.report["fallback"] is None
+    # slow mode (1.80 ms) but the long-chunk plan tuned at 1.78 ms: switching gains nothing
+    t._safe_ms = 1.78
+    t._durations = [1.80] * PlanTuner.WATCH
     t._check_window()
     assert t.monitoring and not calls and t.report["fallback"] is None
     # slow mode (1.95 ms): fall back to the long-chunk candidate 0
@@ -223,3 +230,63 @@ def test_comm_boundary_checks_without_a_gpu():
     assert (r.value, n.value, e.value, t.value) == (1, 4, 0, 0)
     assert L.lope_halo_exchange_end(h, None) == 0                   # nothing pending
     assert L.lope_comm_destroy(h) == 0
+
+
+def _sass_opcodes(kir, dt):
+    """NVRTC-compile (no GPU) into a scratch cache and list the tiled kernels' SASS opcodes."""
+    import collections
+    import pathlib
+    import shutil
+    import subprocess
+    import tempfile
+    if shutil.which("cuobjdump") is None and not pathlib.Path("/usr/local/cuda/bin/cuobjdump").exists():
+        pytest.skip("cuobjdump not available")
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    tmp = tempfile.mkdtemp()
+    try:
+        _lib.lib().lope_set_cache_dir(tmp.encode())
+        h = _lib.compile_kernel(serialize(kir), dt)
+        _lib.destroy_kernel(h)
+        ops = collections.Counter()
+        for f in pathlib.Path(tmp).glob("*.cubin"):
+            for fun in ("lope_tiled", "lope_tiled_multi", "lope_tblock", "lope_row"):
+                out = subprocess.run([exe, "-sass", "-fun", fun, str(f)], capture_output=True, text=True).stdout
+                for m in re.finditer(r"/\*[0-9a-f]{4}\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_]+)", out):
+                    ops[m.group(2)] += 1
+        return ops
+    finally:
+        _lib.lib().lope_set_cache_dir(str(_lib.CACHE_DIR).encode())
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+@pytest.mark.parametrize("name", ["lap3d7", "heat2d", "ninept2d", "laplacian", "drift2"])
+def test_no_contraction_in_kernels_without_division(name):
+    """The parity contract forbids fusing a product into a following add (numpy rounds
+    each node).  fp32 bodies evaluate point pairs with FADD2 / FMUL2; ptxas would fuse
+    a paired multiply by a power of two into FFMA2 -- codegen emits those as scalar
+    multiplies.  Kernels without a division (whose exact reciprocal step uses FMA on
+    purpose) must contain no FFMA / FFMA2 / DFMA at all, and the fp32 ones do pair."""
+    kir = stencils.by_name(name)
+    for dt in ("f32", "f64"):
+        ops = _sass_opcodes(kir, dt)
+        assert sum(ops.values()) > 100, ops
+        for op in ("FFMA", "FFMA2", "DFMA"):
+            assert ops.get(op, 0) == 0, (name, dt, op, ops.get(op))
+        if dt == "f32" and kir.rank >= 2:
+            assert ops.get("FADD2", 0) > 0, (name, ops)
+
+
+def test_no_paired_fma_in_any_golden_random_kernel(golden_random):
+    """No kernel of the golden random set (divisions, scalars, locals, min/max/abs/sqrt)
+    compiles to FFMA2 in fp32: a paired FMA can only come from contraction."""
+    from paper_1502_03504_b200.ir import deserialize
+    meta, _ = golden_random
+    n = 0
+    for m in meta[::2]:
+        kir = deserialize(m["ir"])
+        if kir.rank < 2:
+            continue
+        ops = _sass_opcodes(kir, "f32")
+        assert ops.get("FFMA2", 0) == 0, (m["trial"], m["source"])
+        n += 1
+    assert n >= 20
