@@ -319,7 +319,7 @@ struct DevMod {
   int tiled_smem = 0, tiled_threads = 0, boxx = 0, boxy = 0, tiled_blocks = 0;
   int tiled_local = 0;                  // local memory (spills) per thread of the tiled kernel
   CUfunction tiledm = nullptr;          // multi-array tiled kernel, variant 0 only
-  int tm_smem = 0, tm_threads = 0, tm_boxx = 0, tm_boxy = 0, tm_blocks = 0;
+  int tm_smem = 0, tm_threads = 0, tm_boxx = 0, tm_boxy = 0, tm_blocks = 0, tm_by = 0;
   CUfunction tblock = nullptr;          // temporal blocking (rank 2), variant 0 only
   int tb_smem = 0, tb_tx = 0, tb_ty = 0, tb_tt = 0, tb_threads = 0;
 };
@@ -502,35 +502,50 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
     // several arrays: one TMA box per array per plane (lope_tiled_multi_impl); ring as
     // deep as fits next to NA boxes per stage
     const int na = (int)k.arrays.size();
-    const int ry = k.rank == 3 ? 1 : 2;
-    int ns = 12;
-    auto fits = [&](int n) {
-      const int sz = K->dtype == LOPE_F32 ? 4 : 8, vx = 16 / sz;
-      int un0 = 0, up0 = 0, un1 = 0, up1 = 0, un2 = 0, up2 = 0;
-      for (int a = 0; a < na; ++a) {
-        un0 = std::max(un0, k.fn[a][0]); up0 = std::max(up0, k.fp[a][0]);
-        un1 = std::max(un1, k.fn[a][1]); up1 = std::max(up1, k.fp[a][1]);
-        un2 = std::max(un2, k.fn[a][2]); up2 = std::max(up2, k.fp[a][2]);
-      }
-      const int boxx = ((un0 + vx - 1) / vx) * vx + 32 * vx + ((up0 + vx - 1) / vx) * vx;
-      const int boxy = 16 * ry + un1 + up1;
-      if (boxx > 256 || boxy > 256) return false;
-      const int box = ((boxx * boxy * sz + 127) / 128) * 128;
-      return n >= un2 + up2 + 2 && n * na * box + 16 * n <= 225 * 1024;
-    };
-    while (ns > 2 && !fits(ns)) --ns;
-    if (fits(ns)) {
-      int mpw = k.rank == 2 ? 1 : 0;   // 2-D: a dedicated producer warp (as for one array)
-      if (const char* e = std::getenv("LOPE_MULTI_PW")) mpw = std::atoi(e) ? 1 : 0;
-      s << "typedef LopeTiledMCfg<LopeBody, LT, 1, 16, " << ry << ", " << ns << ", " << mpw << "> LopeMCfg;\n";
-      s << "extern \"C\" __constant__ int lope_tiledm_info[4] = {LopeMCfg::SMEM_BYTES, LopeMCfg::THREADS, "
-           "LopeMCfg::BOXX, LopeMCfg::BOXY};\n";
-      s << "extern \"C\" __global__ void __launch_bounds__(LopeMCfg::THREADS, 1) lope_tiled_multi("
-           "const __grid_constant__ LopeTmapPack<" << na << "> maps, const __grid_constant__ LopeArrPackT<LT, "
-        << na << "> arrs, const LopeScal<LT> sc, const LopeGeom g) {\n"
-        << "  lope_tiled_multi_impl<LopeBody, LT, 1, 16, " << ry << ", " << ns << ", " << mpw
-        << ">(&maps, arrs, sc, g);\n}\n";
+    // a dedicated TMA producer warp (measured: two-array 3-D kernel 1024^3 2.19 ms with 16
+    // compute warps, 2.46 with 15, 3.17 in-band).  17 warps cap registers at 96: the 2-D
+    // window (two rows per lane) spills there, so 2-D runs 15 compute warps (128 registers)
+    int mpw = 1;
+    if (const char* e = std::getenv("LOPE_MULTI_PW")) mpw = std::atoi(e) ? 1 : 0;
+    int wym = 16;
+    const int sz = K->dtype == LOPE_F32 ? 4 : 8, vx = 16 / sz;
+    int un0 = 0, up0 = 0, un1 = 0, up1 = 0, un2 = 0, up2 = 0;
+    for (int a = 0; a < na; ++a) {
+      un0 = std::max(un0, k.fn[a][0]); up0 = std::max(up0, k.fp[a][0]);
+      un1 = std::max(un1, k.fn[a][1]); up1 = std::max(up1, k.fp[a][1]);
+      un2 = std::max(un2, k.fn[a][2]); up2 = std::max(up2, k.fp[a][2]);
     }
+    // emits lope_tiled_multi<suffix> with `ry` rows per lane; get_mod takes the first
+    // one that neither spills nor fails to fit
+    auto emit = [&](const char* suffix, int ry, int wym) {
+      auto fits = [&](int n) {
+        const int boxx = ((un0 + vx - 1) / vx) * vx + 32 * vx + ((up0 + vx - 1) / vx) * vx;
+        const int boxy = wym * ry + un1 + up1;
+        if (boxx > 256 || boxy > 256) return false;
+        const int box = ((boxx * boxy * sz + 127) / 128) * 128;
+        return n >= un2 + up2 + 2 && n * na * box + 16 * n <= 225 * 1024;
+      };
+      int ns = 12;
+      while (ns > 2 && !fits(ns)) --ns;
+      if (!fits(ns)) return;
+      s << "typedef LopeTiledMCfg<LopeBody, LT, 1, " << wym << ", " << ry << ", " << ns << ", " << mpw
+        << "> LopeMCfg" << suffix << ";\n";
+      s << "extern \"C\" __constant__ int lope_tiledm" << suffix << "_info[5] = {LopeMCfg" << suffix
+        << "::SMEM_BYTES, LopeMCfg" << suffix << "::THREADS, LopeMCfg" << suffix << "::BOXX, LopeMCfg" << suffix
+        << "::BOXY, LopeMCfg" << suffix << "::BY};\n";
+      s << "extern \"C\" __global__ void __launch_bounds__(LopeMCfg" << suffix << "::THREADS, 1) lope_tiled_multi"
+        << suffix << "(const __grid_constant__ LopeTmapPack<" << na
+        << "> maps, const __grid_constant__ LopeArrPackT<LT, " << na
+        << "> arrs, const LopeScal<LT> sc, const LopeGeom g) {\n"
+        << "  lope_tiled_multi_impl<LopeBody, LT, 1, " << wym << ", " << ry << ", " << ns << ", " << mpw
+        << ">(&maps, arrs, sc, g);\n}\n";
+    };
+    const int ry = k.rank == 3 ? 1 : 2;
+    const int wy0 = (mpw && k.rank == 2) ? 15 : 16;
+    emit("", ry, wy0);
+    // the register window (arrays x planes x rows x columns) may spill: one row per lane
+    // and 15 + 1 warps (128 registers) as the alternative get_mod falls back to
+    if (ry > 1 || (mpw && wy0 == 16)) emit("_r1", 1, mpw ? 15 : 16);
   }
   if (with_tblock && k.rank == 2 && k.arrays.size() == 1 && k.fn[0][0] <= 4 && k.fp[0][0] <= 4) {
     // 256 x 28 fp32 tiles: 1024^2 splits into 4 x 37 = 148 CTAs, one per SM (config 1);
@@ -656,17 +671,26 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
     int lb = 0;
     if (d.funcGetAttribute(&lb, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, m.tiled) == CUDA_SUCCESS) m.tiled_local = lb;
   }
-  if (d.moduleGetFunction(&m.tiledm, m.mod, "lope_tiled_multi") == CUDA_SUCCESS) {
+  m.tiledm = nullptr;
+  for (const char* suffix : {"", "_r1"}) {
+    if (m.tiledm) break;
+    const std::string fname = std::string("lope_tiled_multi") + suffix;
+    const std::string iname = std::string("lope_tiledm") + suffix + "_info";
+    if (d.moduleGetFunction(&m.tiledm, m.mod, fname.c_str()) != CUDA_SUCCESS) {
+      m.tiledm = nullptr;
+      continue;
+    }
     CUdeviceptr gp;
     size_t gsz;
-    r = d.moduleGetGlobal(&gp, &gsz, m.mod, "lope_tiledm_info");
+    r = d.moduleGetGlobal(&gp, &gsz, m.mod, iname.c_str());
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetGlobal(lope_tiledm_info)");
-    int info[4];
+    int info[5];
     CUDA_TRY(cudaMemcpy(info, (const void*)gp, sizeof info, cudaMemcpyDeviceToHost));
     m.tm_smem = info[0];
     m.tm_threads = info[1];
     m.tm_boxx = info[2];
     m.tm_boxy = info[3];
+    m.tm_by = info[4];
     int nb = 0;
     if (d.funcSetAttribute(m.tiledm, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, m.tm_smem) != CUDA_SUCCESS ||
         d.occupancy(&nb, m.tiledm, m.tm_threads, m.tm_smem) != CUDA_SUCCESS || nb < 1)
@@ -678,8 +702,6 @@ int get_mod(lope_kernel* K, int vi, DevMod** out) {
         lb > 0 && !std::getenv("LOPE_MULTI_ALLOW_SPILL"))
       m.tiledm = nullptr;
     m.tm_blocks = nb;
-  } else {
-    m.tiledm = nullptr;
   }
   if (d.moduleGetFunction(&m.tblock, m.mod, "lope_tblock") == CUDA_SUCCESS) {
     CUdeviceptr gp;
@@ -818,7 +840,15 @@ int encode_tmap_box(const lope_layout* L, const void* base, int boxx, int boxy, 
 }
 
 int zchunk_default(const lope::Kir& k) {
-  if (k.rank < 3) return 1;
+  if (k.rank < 2) return 1;
+  if (k.rank == 2) {
+    // y tiles per unit (the tiled kernel streams rank-2 units along y)
+    if (const char* e = std::getenv("LOPE_YCHUNK")) {
+      int v = std::atoi(e);
+      if (v > 0) return v;
+    }
+    return 8;
+  }
   if (const char* e = std::getenv("LOPE_ZCHUNK")) {
     int v = std::atoi(e);
     if (v > 0) return v;
@@ -937,6 +967,11 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     long long ntx = (g.ext[0] + 32 * vx * c.bxw - 1) / (32 * vx * c.bxw);
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
+    if (k.rank == 2) {
+      // rank 2 streams units along y: `zchunk` y tiles per unit (lope_tiled_impl, YS)
+      nty = (nty + g.zchunk - 1) / g.zchunk;
+      nzc = 1;
+    }
     long long units = ntx * nty * nzc;
     if (units >= (1LL << 31)) return fail(108, "launch range too large for the tiled path");
     long long grid = (long long)m->tiled_blocks * sm_count();
@@ -1019,9 +1054,8 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     }
     const int padx = ((un0 + vx - 1) / vx) * vx;
     g.box0 = (int)(L->base + L->lo[0] + r0x - padx);
-    const int ry = k.rank == 3 ? 1 : 2;
     long long ntx = (g.ext[0] + 32 * vx - 1) / (32 * vx);
-    long long nty = (ext[1] + 16 * ry - 1) / (16 * ry);
+    long long nty = (ext[1] + m->tm_by - 1) / m->tm_by;
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     long long units = ntx * nty * nzc;
     if (units >= (1LL << 31)) return fail(108, "launch range too large for the tiled path");
@@ -1491,15 +1525,16 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
     }
   } else {
     // 2-D: the dedicated producer always won (ninept2d 16384^2: 0.355 vs 0.50 ms in-band),
-    // so only the ring depth varies; an in-band default (wide fp64 boxes) may try one
-    c.push_back({base, 1, 0});
+    // so the ring depth and the y tiles per unit vary; an in-band default (wide fp64
+    // boxes) may try one
+    for (int yc : {1, 8, 32}) c.push_back({base, yc, 0});
     TileCfg t = base;
     t.ns = base.ns == 8 ? 12 : 8;
-    c.push_back({t, 1, 0});
+    for (int yc : {8, 32}) c.push_back({t, yc, 0});
     if (base.pw == 0) {
       t = base;
       t.pw = 1;
-      c.push_back({t, 1, 0});
+      for (int yc : {8, 32}) c.push_back({t, yc, 0});
     }
   }
   return c;

@@ -264,7 +264,13 @@ struct Emitter {
         return "rd.template at<" + std::to_string(n.arr) + "," + std::to_string(n.off[0]) + "," +
                std::to_string(n.off[1]) + "," + std::to_string(n.off[2]) + ">()";
       }
-      case Node::ADD: return "AR::add(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      case Node::ADD: {
+        // a + (-b) is a - b in IEEE arithmetic (same rounding, same signed zeros): one
+        // subtraction instead of a negation feeding an add (FADD2 takes the negated operand)
+        const Node& b = k.nodes[n.kids[1]];
+        if (b.kind == Node::NEG) return "AR::sub(" + ex(n.kids[0]) + ", " + ex(b.kids[0]) + ")";
+        return "AR::add(" + ex(n.kids[0]) + ", " + ex(n.kids[1]) + ")";
+      }
       case Node::MUL: {
         // a product with a power-of-two constant is exact unless it underflows, and ptxas
         // then fuses a paired multiply into the following paired add (FFMA2), which

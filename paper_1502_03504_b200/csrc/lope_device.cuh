@@ -39,6 +39,7 @@ template <> struct LopeAr<float> {
   static __device__ __forceinline__ float min_(float a, float b) { return lope_min<float>(a, b); }
   static __device__ __forceinline__ float max_(float a, float b) { return lope_max<float>(a, b); }
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float mulx(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
@@ -99,6 +100,7 @@ template <> struct LopeAr<double> {
   static __device__ __forceinline__ double min_(double a, double b) { return lope_min<double>(a, b); }
   static __device__ __forceinline__ double max_(double a, double b) { return lope_max<double>(a, b); }
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double mulx(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
@@ -113,7 +115,7 @@ template <> struct LopeAr<double> {
       const double q = __dmul_rn(x, y);
       const double r = __fma_rn(-q, b, x);
       const double m = __fma_rn(r, y, q);
-#ifndef LOPE_DIVC_DSETP
+#ifdef LOPE_DIVC_INTCLASS
       bool inr, special;
       classify(x, inr, special);
       slow |= (y != y) || !(inr | special);
@@ -149,7 +151,7 @@ template <> struct LopeAr<double> {
       const double q = __dmul_rn(x, yd);
       const double r = __fma_rn(-q, b, x);
       const double m = __fma_rn(r, yd, q);
-#ifndef LOPE_DIVC_DSETP
+#ifdef LOPE_DIVC_INTCLASS
       bool inr, special;
       classify(x, inr, special);
       slow |= !(inr | special);
@@ -184,6 +186,13 @@ struct LopeAr2 {
     W d;
     asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
         "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+  }
+  static __device__ __forceinline__ W sub(W a, W b) {
+    W d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
         : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
   }
@@ -519,17 +528,19 @@ struct LopeVecOut {
     xm = 0;
 #pragma unroll
     for (int e = 0; e < VX; ++e) xm |= (x + e >= g.xshift && x + e < g.ext[0]) ? (1u << e) : 0u;
+    // opaque to the optimiser: otherwise ptxas rematerialises the per-element range
+    // tests inside the plane loop (6+ ISETP per row store on the all-inside path)
+    asm volatile("mov.b32 %0, %0;" : "+r"(xm));
   }
-  // the vector itself (element stores only where it straddles an end of the range)
+  // the vector itself (element stores only where it straddles an end of the range);
+  // predicated stores, no branch: a branch here costs a convergence barrier pair per row
   __device__ __forceinline__ void put(T* p, const V& o) const {
-    if (xm == ALL) {
-      *reinterpret_cast<V*>(p) = o;
-    } else {
-      const T* oe = reinterpret_cast<const T*>(&o);
+    const bool full = xm == ALL;
+    if (full) *reinterpret_cast<V*>(p) = o;
+    const T* oe = reinterpret_cast<const T*>(&o);
 #pragma unroll
-      for (int e = 0; e < VX; ++e)
-        if ((xm >> e) & 1u) p[e] = oe[e];
-    }
+    for (int e = 0; e < VX; ++e)
+      if (!full && ((xm >> e) & 1u)) p[e] = oe[e];
   }
   // its x images (xw lanes only)
   __device__ __forceinline__ void putx(T* p, const V& o, const LopeGeom& g) const {
@@ -546,28 +557,22 @@ struct LopeVecOut {
     }
   }
   // the vector at p (row yg of the range, plane with z-image flag zw / offset zimg)
-  // with every image: x, y, z and their combinations
+  // with every image: x, y, z and their combinations.  A rolled loop over the (up to
+  // four) row targets keeps one copy of the store code: this path runs for boundary
+  // rows and planes only, and the kernel's hot loop stays small in the i-cache.
   __device__ __forceinline__ void store_all(T* p, const V& o, int yg, bool zw, lope_i64 zimg, lope_i64 s1,
                                             const LopeGeom& g) const {
-    put(p, o);
-    if (xw) putx(p, o, g);
     const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
-    if (yw | zw) {
-      // y images (rank 2: the slowest dim, possibly in a neighbour's block)
-      const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdl : 0)
-                                          : -(lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdh : 0));
-      if (yw) {
-        put(p + yimg, o);
-        if (xw) putx(p + yimg, o, g);
-      }
-      if (zw) {
-        put(p + zimg, o);
-        if (xw) putx(p + zimg, o, g);
-        if (yw) {
-          put(p + zimg + yimg, o);
-          if (xw) putx(p + zimg + yimg, o, g);
-        }
-      }
+    // y images (rank 2: the slowest dim, possibly in a neighbour's block)
+    const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdl : 0)
+                                        : -(lope_i64)g.m[1] * s1 + (RANK == 2 ? g.sdh : 0));
+    const int nt = (yw | zw) ? 4 : 1;
+#pragma unroll 1
+    for (int t = 0; t < nt; ++t) {
+      if (((t & 1) && !yw) || ((t & 2) && !zw)) continue;
+      T* q = p + ((t & 1) ? yimg : 0) + ((t & 2) ? zimg : 0);
+      put(q, o);
+      if (xw) putx(q, o, g);
     }
   }
 };
@@ -780,12 +785,17 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   lope_u64* full = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
   lope_u64* empty = full + NS;
 
+  // Rank 2 streams along y: a unit is an x tile and `zchunk` consecutive y tiles (each
+  // one "plane" of the ring: its box re-reads the tile's y halo rows), so the per-unit
+  // setup is paid once per chunk instead of once per tile.  Rank 3 streams along z.
+  constexpr bool YS = Body::RANK == 2;
   const int ntx = (g.ext[0] + C::BX - 1) / C::BX;
   const int nty = (g.ext[1] + C::BY - 1) / C::BY;
   const int zc = g.zchunk;
-  const int nzc = (g.ext[2] + zc - 1) / zc;
-  const int nunits = ntx * nty * nzc;     // < 2^31 (host checks)
-const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
+  const int nyu = YS ? (nty + zc - 1) / zc : nty;          // y units per x tile column
+  const int nzc = YS ? 1 : (g.ext[2] + zc - 1) / zc;
+  const int nunits = ntx * nyu * nzc;     // < 2^31 (host checks)
+  const int yb = (g.yband > 0 && nyu % g.yband == 0) ? g.yband : nyu;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -821,9 +831,9 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
     pw.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
     if (p_u < nunits) {
       const int z0 = pw.zi * zc;
-      p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+      p_nl = YS ? min(zc, nty - pw.ty() * zc) : min(zc, g.ext[2] - z0) + NZW - 1;
       p_bx = g.box0 + pw.tx * C::BX;
-      p_by = oy + pw.ty() * C::BY;
+      p_by = oy + (YS ? pw.ty() * zc : pw.ty()) * C::BY;
       p_z = oz + z0;
     }
   }
@@ -841,10 +851,12 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
         else if (!lope_mbar_test(&empty[slot], par)) break;
       }
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
+      const int ly = YS ? p_by + p_pl * C::BY : p_by;      // this plane's box origin
+      const int lz = YS ? p_z : p_z + p_pl;
       if (g.p1 > 0)
-        lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
+        lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, ly + lz * g.p1);
       else
-        lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by, p_z + p_pl);
+        lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, ly, lz);
       ++p_L;
       if (++p_slot == NS) { p_slot = 0; ++p_round; }
       if (++p_pl == p_nl) {
@@ -853,9 +865,9 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
         pw.next();
         if (p_u < nunits) {
           const int z0 = pw.zi * zc;
-          p_nl = min(zc, g.ext[2] - z0) + NZW - 1;
+          p_nl = YS ? min(zc, nty - pw.ty() * zc) : min(zc, g.ext[2] - z0) + NZW - 1;
           p_bx = g.box0 + pw.tx * C::BX;
-          p_by = oy + pw.ty() * C::BY;
+          p_by = oy + (YS ? pw.ty() * zc : pw.ty()) * C::BY;
           p_z = oz + z0;
         }
       }
@@ -888,58 +900,70 @@ const int yb = (g.yband > 0 && nty % g.yband == 0) ? g.yband : nty;
   lope_u32 lbase = 0;     // (the in-band producer's "needed" bound)
   for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
     const int z0 = w.zi * zc;
-    const int nz = min(zc, g.ext[2] - z0);
+    const int nz = YS ? min(zc, nty - w.ty() * zc) : min(zc, g.ext[2] - z0);
     const int x = w.tx * C::BX + cx;
-    const int ybase = w.ty() * C::BY + row0;
+    int ybase = (YS ? w.ty() * zc : w.ty()) * C::BY + row0;
     const bool xok = x < g.ext[0];
-    const int nrow = min(RY, g.ext[1] - ybase);
+    int nrow = min(RY, g.ext[1] - ybase);
     // stores and periodic images (lope_step) of this lane's vector (LopeVecOut)
     LopeVecOut<T, Body::RANK> vo;
     vo.init(x, xok, g);
     const bool wx_any = __any_sync(0xffffffffu, vo.xw);
-    const bool wy_any = (g.wrap & 2) && (nrow > 0) &&
-                        (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
-                         lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
+    bool wy_any = (g.wrap & 2) && (nrow > 0) &&
+                  (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                   lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
     T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
-    for (int pz = 0; pz < nz; ++pz, orow += s2) {
-      // ---- top up the TMA ring (warp 0 lane 0) ----
-      if (!PW && warp == 0) {
+    const lope_i64 pstep = YS ? (lope_i64)C::BY * s1 : s2;   // output offset of the next plane
+    // ---- unit prologue: top up the ring, wait for the window's older planes and load
+    // the z history of the first plane (planes z0-1 .. z0-FZN at own points) ----
+    if (!PW && warp == 0) {
+      if (lane == 0) produce(NB ? lbase + NZW : 0xffffffffu, lbase + NS);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k + 1 < NZW; ++k) {
+      int sl = c_slot + k;
+      lope_u32 ph = c_par;
+      if (sl >= NS) { sl -= NS; ph ^= 1u; }
+      lope_mbar_wait_addr(full_a + 8u * sl, ph);
+      if (ZHIST && k < FZN) {
+        const T* hp = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const V vv = *reinterpret_cast<const V*>(hp + (Body::FN1 + r) * C::BOXX);
+          const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) hist[FZN - 1 - k][r][e] = ve[e];
+        }
+      }
+    }
+    for (int pz = 0; pz < nz; ++pz, orow += pstep) {
+      if (YS && pz > 0) {
+        ybase += C::BY;
+        nrow = min(RY, g.ext[1] - ybase);
+        wy_any = (g.wrap & 2) && (nrow > 0) &&
+                 (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                  lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
+      }
+      // ---- top up the TMA ring (warp 0 lane 0; the unit's first plane: prologue) ----
+      if (!PW && warp == 0 && pz > 0) {
         if (lane == 0)
-          produce(NB ? lbase + pz + NZW : 0xffffffffu,
-                  (ZHIST ? (pz == 0 ? lbase : lbase + pz + FZN) : lbase + pz) + NS);
+          produce(NB ? lbase + pz + NZW : 0xffffffffu, (ZHIST ? lbase + pz + FZN : lbase + pz) + NS);
         __syncwarp();
       }
-      // ---- wait for the planes this iteration reads ----
-      // The window slides by one plane: after the unit's first plane only the newest
-      // plane has not been waited for (a slot cannot be refilled while this warp holds
-      // it, so an earlier completed phase stays complete).
+      // ---- the planes this iteration reads; wait for the newest only ----
+      // The window slides by one plane: the unit prologue waited for the others (a slot
+      // cannot be refilled while this warp holds it, so a completed phase stays complete).
       const T* sp[NZW];
       int ks[NZW];
-      lope_u32 kp[NZW];
 #pragma unroll
       for (int k = 0; k < NZW; ++k) {
         int sl = c_slot + k;
         lope_u32 ph = c_par;
         if (sl >= NS) { sl -= NS; ph ^= 1u; }
         ks[k] = sl;
-        kp[k] = ph;
         sp[k] = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
-        const bool need = pz == 0 ? !(ZHIST && k < FZN) : (k == NZW - 1);
-        if (need) lope_mbar_wait_addr(full_a + 8u * sl, ph);
-      }
-      if (ZHIST && pz == 0) {
-        // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
-#pragma unroll
-        for (int d = 0; d < FZN; ++d) {
-          lope_mbar_wait_addr(full_a + 8u * ks[FZN - 1 - d], kp[FZN - 1 - d]);
-#pragma unroll
-          for (int r = 0; r < RY; ++r) {
-            const V vv = *reinterpret_cast<const V*>(sp[FZN - 1 - d] + (Body::FN1 + r) * C::BOXX);
-            const T* ve = reinterpret_cast<const T*>(&vv);
-#pragma unroll
-            for (int e = 0; e < VX; ++e) hist[d][r][e] = ve[e];
-          }
-        }
+        if (k == NZW - 1) lope_mbar_wait_addr(full_a + 8u * sl, ph);
       }
       // ---- register window, filled row by row and consumed as soon as a row of
       // outputs has all its inputs (short live ranges: no spills at 16 warps) ----

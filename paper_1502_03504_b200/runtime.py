@@ -302,7 +302,7 @@ class PlanTuner:
         ci = min(best, key=best.get)
         self._set(*self.cands[ci])
         safe = [c for c in best if self.cands[c][1] >= self.SAFE_ZCHUNK]
-        if self.cands[ci][1] < self.SAFE_ZCHUNK and safe:
+        if self.layout.rank == 3 and self.cands[ci][1] < self.SAFE_ZCHUNK and safe:
             cs = min(safe, key=best.get)
             self._safe = (cs, min(acc[ci]))     # the winner's fastest trial: its fast mode
             self._safe_ms = best[cs]            # what the long-chunk plan itself costs

@@ -478,6 +478,9 @@ def test_multi_array_tiled_equals_generic(monkeypatch, rank, na, dt):
         R.launch(k, hs, sub)
         outs.append([h.get_padded() for h in hs])
         monkeypatch.delenv("LOPE_FORCE_GENERIC", raising=False)
+        if not generic:   # the multi-array kernel itself ran (no silent generic fallback)
+            n = json.loads(k.describe())["launches"]
+            assert n["tiled_multi"] == 2 and n["generic"] == 0, n
     for a_, b_ in zip(*outs):
         assert O.equal_bits(a_, b_)
 
