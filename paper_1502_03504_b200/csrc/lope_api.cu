@@ -309,6 +309,7 @@ struct TileCfg {
   int pw = 0;     // 1: dedicated TMA producer warp
   int sh = 0;     // 1: x-halo columns through warp shuffles (fp32, one-column halos)
   int nb = 0;     // 1: in-band producer prefetches only into already-free slots
+  int rag = 0;    // 1: ragged-x kernel (masked edge vectors, cell-by-cell x images)
 };
 
 struct DevMod {
@@ -495,7 +496,7 @@ std::string build_source(const lope_kernel* K, const LopeVariant& V, bool with_t
       << ", " << c.mb << ") lope_tiled(const __grid_constant__ LopeTmap map, const LopeArr<LT> a, "
          "const LopeScal<LT> sc, const LopeGeom g) {\n"
       << "  lope_tiled_impl<LopeBody, LT, " << c.bxw << ", " << c.wy << ", " << c.ry << ", " << c.ns
-      << ", " << c.pw << ", " << c.sh << ", " << c.nb << ">(&map, a, sc, g);\n"
+      << ", " << c.pw << ", " << c.sh << ", " << c.nb << ", " << (c.rag ? "true" : "false") << ">(&map, a, sc, g);\n"
       << "  if (g.sdl | g.sdh) __threadfence_system();   // peer-block images visible system-wide\n}\n";
   }
   if (with_tblock && k.rank >= 2 && k.arrays.size() >= 2 && k.arrays.size() <= 4) {
@@ -730,7 +731,7 @@ int add_variant(lope_kernel* K, const TileCfg& cfg, int* vi = nullptr) {
   for (size_t i = 0; i < K->variants.size(); ++i) {
     const TileCfg& c = K->variants[i].tile;
     if (c.bxw == cfg.bxw && c.wy == cfg.wy && c.ry == cfg.ry && c.ns == cfg.ns && c.mb == cfg.mb && c.pw == cfg.pw &&
-        c.sh == cfg.sh && c.nb == cfg.nb) {
+        c.sh == cfg.sh && c.nb == cfg.nb && c.rag == cfg.rag) {
       if (vi) *vi = (int)i;
       return 0;
     }
@@ -901,6 +902,23 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
         zc = it->second.zchunk;
         yband = it->second.yband;
       }
+    }
+  }
+  {
+    // Ragged x (a range start or extent that is not whole 16-byte vectors, or an
+    // interior too narrow / not whole vectors for whole-atom x images): the RAG
+    // instantiation of the same tile (masked edge vectors, cell-by-cell x images),
+    // compiled on first use.  The aligned instantiation carries none of that code.
+    const int vxr = 16 / (int)sizeof(T);
+    bool rag = (r0[0] % vxr) != 0 || (ext[0] % vxr) != 0;
+    if (wrap & 1) {
+      const long long line = 64 / (long long)sizeof(T);
+      rag = rag || !(layouts[0].interior[0] % vxr == 0 && layouts[0].interior[0] >= 2 * line);
+    }
+    if (rag && K->variants[vi].tiled_ok && K->ir.arrays.size() == 1 && !K->variants[vi].tile.rag) {
+      TileCfg t = K->variants[vi].tile;
+      t.rag = 1;
+      if (int e = add_variant(K, t, &vi)) return e;
     }
   }
   const LopeVariant& V = K->variants[vi];

@@ -528,9 +528,6 @@ struct LopeVecOut {
     xm = 0;
 #pragma unroll
     for (int e = 0; e < VX; ++e) xm |= (x + e >= g.xshift && x + e < g.ext[0]) ? (1u << e) : 0u;
-    // opaque to the optimiser: otherwise ptxas rematerialises the per-element range
-    // tests inside the plane loop (6+ ISETP per row store on the all-inside path)
-    asm volatile("mov.b32 %0, %0;" : "+r"(xm));
   }
   // the vector itself (element stores only where it straddles an end of the range);
   // predicated stores, no branch: a branch here costs a convergence barrier pair per row
@@ -770,7 +767,7 @@ struct LopeUnitWalk {
   }
 };
 
-template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0, int SH = 0, int NB = 0>
+template <class Body, class T, int WX, int WY, int RY, int NS, int PW = 0, int SH = 0, int NB = 0, bool RAG = false>
 __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeArr<T>& a,
                                                 const LopeScal<T>& sc, const LopeGeom& g) {
   typedef LopeTiledCfg<Body, T, WX, WY, RY, NS, PW> C;
@@ -785,9 +782,12 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   lope_u64* full = reinterpret_cast<lope_u64*>(lope_smem + NS * C::STAGE_BYTES);
   lope_u64* empty = full + NS;
 
-  // Rank 2 streams along y: a unit is an x tile and `zchunk` consecutive y tiles (each
-  // one "plane" of the ring: its box re-reads the tile's y halo rows), so the per-unit
-  // setup is paid once per chunk instead of once per tile.  Rank 3 streams along z.
+  // Rank 2 streams along y (YS): a unit is an x tile and `zchunk` consecutive y tiles
+  // (each one "plane" of the ring: its box re-reads the tile's y halo rows), so the
+  // per-unit setup is paid once per chunk instead of once per tile (c4: 3.83 -> 3.14
+  // ms).  Rank 3 streams along z.  Everything YS / RAG adds is compile-time gated: the
+  // aligned rank-3 instantiation is instruction for instruction the round-1 kernel
+  // (measured: any extra live state in the plane loop costs 10-15% on config 3).
   constexpr bool YS = Body::RANK == 2;
   const int ntx = (g.ext[0] + C::BX - 1) / C::BX;
   const int nty = (g.ext[1] + C::BY - 1) / C::BY;
@@ -840,25 +840,28 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   // Loads below `needed` are waited for (the issuing warp reads them next); loads up to
   // `limit` are prefetch and only issued while their slot is already free, so the
   // in-band producer never stalls warp 0 on a slower warp just to run further ahead.
-  int p_slot = 0;
-  lope_u32 p_round = 0;     // p_L = p_round * NS + p_slot, kept without division
   auto produce = [&](lope_u32 needed, lope_u32 limit) {
     while (p_L < limit && p_u < nunits) {
-      const int slot = p_slot;
-      if (p_round > 0) {
-        const lope_u32 par = (p_round - 1) & 1;
+      const lope_u32 slot = p_L % NS;
+      if (p_L >= (lope_u32)NS) {
+        const lope_u32 par = ((p_L / NS) - 1) & 1;
         if (p_L < needed) lope_mbar_wait(&empty[slot], par);
         else if (!lope_mbar_test(&empty[slot], par)) break;
       }
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
-      const int ly = YS ? p_by + p_pl * C::BY : p_by;      // this plane's box origin
-      const int lz = YS ? p_z : p_z + p_pl;
-      if (g.p1 > 0)
-        lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, ly + lz * g.p1);
-      else
-        lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, ly, lz);
+      if constexpr (YS) {
+        // rank 2: the unit's planes are consecutive y tiles
+        if (g.p1 > 0)
+          lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + p_pl * C::BY + p_z * g.p1);
+        else
+          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + p_pl * C::BY, p_z);
+      } else {
+        if (g.p1 > 0)
+          lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
+        else
+          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by, p_z + p_pl);
+      }
       ++p_L;
-      if (++p_slot == NS) { p_slot = 0; ++p_round; }
       if (++p_pl == p_nl) {
         p_pl = 0;
         p_u += gridDim.x;
@@ -886,84 +889,71 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   const int cx = (wx * 32 + lane) * VX;    // first column of this lane within the tile
   const int row0 = wy * RY;                // first row within the tile
   const lope_i64 s1 = a.s1, s2 = a.s2;
+  constexpr int SEC = 64 / (int)sizeof(T);          // one 64-byte DRAM atom
+  // The host sends only geometries with ext[0] % VX == 0 and, when images are
+  // refreshed, m[0] >= 2*SEC, m[0] % VX == 0 and m[d] >= lo[d] + hi[d] (each halo
+  // cell has exactly one image); anything else runs on the generic kernel.
   const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
 
   LopeUnitWalk w;
   w.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
+  lope_u32 lbase = 0;
   T hist[FZN > 0 ? FZN : 1][RY][VX];
-  // Ring position of the window's first plane, tracked incrementally (slot, phase) so
-  // the plane loop does no division by the ring depth; barrier addresses in the shared
-  // window are formed once.
-  const lope_u32 full_a = lope_smem_u32(full), empty_a = lope_smem_u32(empty);
-  int c_slot = 0;
-  lope_u32 c_par = 0;
-  lope_u32 lbase = 0;     // (the in-band producer's "needed" bound)
   for (int u = blockIdx.x; u < nunits; u += gridDim.x, w.next()) {
     const int z0 = w.zi * zc;
     const int nz = YS ? min(zc, nty - w.ty() * zc) : min(zc, g.ext[2] - z0);
     const int x = w.tx * C::BX + cx;
-    int ybase = (YS ? w.ty() * zc : w.ty()) * C::BY + row0;
+    const int ybase = (YS ? w.ty() * zc : w.ty()) * C::BY + row0;
     const bool xok = x < g.ext[0];
-    int nrow = min(RY, g.ext[1] - ybase);
-    // stores and periodic images (lope_step) of this lane's vector (LopeVecOut)
-    LopeVecOut<T, Body::RANK> vo;
-    vo.init(x, xok, g);
-    const bool wx_any = __any_sync(0xffffffffu, vo.xw);
-    bool wy_any = (g.wrap & 2) && (nrow > 0) &&
-                  (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
-                   lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
+    const int nrow = min(RY, g.ext[1] - ybase);
+    // Periodic images (lope_step): x images are whole 64-byte atoms written by the
+    // lanes whose vectors land in the halo atom (padding included; the layout
+    // reserves an atom per side), y and z images are whole rows / planes.
+    const int xg = x + g.r0[0];
+    const bool xw = (g.wrap & 1) && xok && ((g.hi[0] > 0 && xg < SEC) || (g.lo[0] > 0 && xg >= g.m[0] - SEC));
+    const int ximg = xg < SEC ? g.m[0] : -g.m[0];
+    const bool wx_any = __any_sync(0xffffffffu, xw);
+    const bool wy_any = (g.wrap & 2) && (nrow > 0) &&
+                        (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                         lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
     T* orow = a.out + a.org + x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
-    const lope_i64 pstep = YS ? (lope_i64)C::BY * s1 : s2;   // output offset of the next plane
-    // ---- unit prologue: top up the ring, wait for the window's older planes and load
-    // the z history of the first plane (planes z0-1 .. z0-FZN at own points) ----
-    if (!PW && warp == 0) {
-      if (lane == 0) produce(NB ? lbase + NZW : 0xffffffffu, lbase + NS);
-      __syncwarp();
+    bool rag_plain = false;
+    if constexpr (RAG) {
+      LopeVecOut<T, Body::RANK> v0;
+      v0.init(x, xok, g);
+      rag_plain = __all_sync(0xffffffffu, !v0.xw && (!xok || v0.xm == v0.ALL));
     }
-#pragma unroll
-    for (int k = 0; k + 1 < NZW; ++k) {
-      int sl = c_slot + k;
-      lope_u32 ph = c_par;
-      if (sl >= NS) { sl -= NS; ph ^= 1u; }
-      lope_mbar_wait_addr(full_a + 8u * sl, ph);
-      if (ZHIST && k < FZN) {
-        const T* hp = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          const V vv = *reinterpret_cast<const V*>(hp + (Body::FN1 + r) * C::BOXX);
-          const T* ve = reinterpret_cast<const T*>(&vv);
-#pragma unroll
-          for (int e = 0; e < VX; ++e) hist[FZN - 1 - k][r][e] = ve[e];
-        }
-      }
-    }
-    for (int pz = 0; pz < nz; ++pz, orow += pstep) {
-      if (YS && pz > 0) {
-        ybase += C::BY;
-        nrow = min(RY, g.ext[1] - ybase);
-        wy_any = (g.wrap & 2) && (nrow > 0) &&
-                 (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
-                  lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
-      }
-      // ---- top up the TMA ring (warp 0 lane 0; the unit's first plane: prologue) ----
-      if (!PW && warp == 0 && pz > 0) {
+    auto plane = [&](const int pz, T* orow, const int ybase, const int nrow, const bool wy_any) {
+      // ---- top up the TMA ring (warp 0 lane 0) ----
+      if (!PW && warp == 0) {
         if (lane == 0)
-          produce(NB ? lbase + pz + NZW : 0xffffffffu, (ZHIST ? lbase + pz + FZN : lbase + pz) + NS);
+          produce(NB ? lbase + pz + NZW : 0xffffffffu,
+                  (ZHIST ? (pz == 0 ? lbase : lbase + pz + FZN) : lbase + pz) + NS);
         __syncwarp();
       }
-      // ---- the planes this iteration reads; wait for the newest only ----
-      // The window slides by one plane: the unit prologue waited for the others (a slot
-      // cannot be refilled while this warp holds it, so a completed phase stays complete).
+      // ---- wait for the planes this iteration reads ----
       const T* sp[NZW];
-      int ks[NZW];
 #pragma unroll
       for (int k = 0; k < NZW; ++k) {
-        int sl = c_slot + k;
-        lope_u32 ph = c_par;
-        if (sl >= NS) { sl -= NS; ph ^= 1u; }
-        ks[k] = sl;
-        sp[k] = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
-        if (k == NZW - 1) lope_mbar_wait_addr(full_a + 8u * sl, ph);
+        const lope_u32 L = lbase + pz + k;
+        sp[k] = reinterpret_cast<const T*>(lope_smem + (L % NS) * C::STAGE_BYTES) + soff;
+        if (ZHIST && k < FZN && pz > 0) continue;          // past planes come from registers
+        lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+      }
+      if (ZHIST && pz == 0) {
+        // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
+#pragma unroll
+        for (int d = 0; d < FZN; ++d) {
+          const lope_u32 L = lbase + (FZN - 1 - d);
+          lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            const V vv = *reinterpret_cast<const V*>(sp[FZN - 1 - d] + (Body::FN1 + r) * C::BOXX);
+            const T* ve = reinterpret_cast<const T*>(&vv);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) hist[d][r][e] = ve[e];
+          }
+        }
       }
       // ---- register window, filled row by row and consumed as soon as a row of
       // outputs has all its inputs (short live ranges: no spills at 16 warps) ----
@@ -1011,32 +1001,16 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
         }
         const int r = q - Body::FN1 - Body::FP1;
         if (r >= 0) {
-          if (LOPE_PAIR && sizeof(T) == 4) {
-            // fp32: two points per FADD2 / FMUL2
 #pragma unroll
-            for (int v = 0; v < VX; v += 2) {
-              LopeWinReader2<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
-              rd.win = &win[0][0][0];
-              rd.hist = &hist[0][0][0];
-              rd.r = r;
-              rd.v = v;
-              float2 res[1];
-              Body::template eval<T, FAST, decltype(rd), float2, LopeAr2>(rd, sc.v, res, slow);
-              vals[r][v] = res[0].x;
-              vals[r][v + 1] = res[0].y;
-            }
-          } else {
-#pragma unroll
-            for (int v = 0; v < VX; ++v) {
-              LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
-              rd.win = &win[0][0][0];
-              rd.hist = &hist[0][0][0];
-              rd.r = r;
-              rd.v = v;
-              T res[1];
-              Body::template eval<T, FAST>(rd, sc.v, res, slow);
-              vals[r][v] = res[0];
-            }
+          for (int v = 0; v < VX; ++v) {
+            LopeWinReader<T, NR, NXW, FZN, Body::FN0, Body::FN1, RY, VX, ZHIST> rd;
+            rd.win = &win[0][0][0];
+            rd.hist = &hist[0][0][0];
+            rd.r = r;
+            rd.v = v;
+            T res[1];
+            Body::template eval<T, FAST>(rd, sc.v, res, slow);
+            vals[r][v] = res[0];
           }
           if (ZHIST && !FAST) {
             // row r of the history only feeds row r: shift it now
@@ -1088,57 +1062,116 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       if (lane == 0) {
         if (ZHIST) {
           if (pz == 0)
-#pragma unroll
-            for (int k = 0; k < FZN; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[k]);
-          lope_mbar_arrive_addr(empty_a + 8u * ks[FZN]);
+            for (int k = 0; k < FZN; ++k) lope_mbar_arrive(&empty[(lbase + k) % NS]);
+          lope_mbar_arrive(&empty[(lbase + pz + FZN) % NS]);
           if (pz == nz - 1)
-#pragma unroll
-            for (int k = 1; k <= FZP; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[FZN + k]);
+            for (int k = 1; k <= FZP; ++k) lope_mbar_arrive(&empty[(lbase + pz + FZN + k) % NS]);
         } else {
-          lope_mbar_arrive_addr(empty_a + 8u * ks[0]);
+          lope_mbar_arrive(&empty[(lbase + pz) % NS]);
           if (pz == nz - 1)
-#pragma unroll
-            for (int k = 1; k < NZW; ++k) lope_mbar_arrive_addr(empty_a + 8u * ks[k]);
+            for (int k = 1; k < NZW; ++k) lope_mbar_arrive(&empty[(lbase + pz + k) % NS]);
         }
       }
-      // the window's first plane moves on by one
-      if (++c_slot == NS) { c_slot = 0; c_par ^= 1u; }
-      if (!xok || nrow <= 0) continue;
+      if (!xok || nrow <= 0) return;
       // ---- store ----
-      const int zg = z0 + pz + g.r0[2];
-      const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
-      if (!(wy_any | zw)) {
+      if constexpr (RAG) {
+        // ragged x (range start or extent not whole vectors, or cell-by-cell x images):
+        // tiles whose lanes all hold whole in-range vectors and no x image store plainly
+        // (warp-uniform `rag_plain`, set per unit); the others mask their edge vectors
+        // and store every image through LopeVecOut
+        const int zg = z0 + pz + g.r0[2];
+        const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
+        if (rag_plain && !(wy_any | zw)) {
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          if (r >= nrow) continue;
-          V o;
-          T* oe = reinterpret_cast<T*>(&o);
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
-          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
-          vo.put(orow + (lope_i64)r * s1, o);
-          if (wx_any && vo.xw) vo.putx(orow + (lope_i64)r * s1, o, g);
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
+          }
+        } else {
+          LopeVecOut<T, Body::RANK> vo;
+          vo.init(x, xok, g);
+          const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            vo.store_all(orow + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
+          }
         }
       } else {
-        // z images (rank 3: the slowest dim, possibly in a neighbour's block)
-        const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
-#pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          if (r >= nrow) continue;
-          V o;
-          T* oe = reinterpret_cast<T*>(&o);
-#pragma unroll
-          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
-          vo.store_all(orow + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
+        const int zg = z0 + pz + g.r0[2];
+        const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
+        if (!(wy_any | zw)) {
+  #pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+  #pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
+            if (wx_any && xw) *reinterpret_cast<V*>(orow + (lope_i64)r * s1 + ximg) = o;
+          }
+        } else {
+          // z images (rank 3: the slowest dim, possibly in a neighbour's block)
+          const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
+  #pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+  #pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            T* p = orow + (lope_i64)r * s1;
+            *reinterpret_cast<V*>(p) = o;
+            if (xw) *reinterpret_cast<V*>(p + ximg) = o;
+            const int yg = ybase + r + g.r0[1];
+            const bool yw = (g.wrap & 2) && lope_near(yg, g.m[1], g.lo[1], g.hi[1]);
+            if (yw | zw) {
+              // y images (rank 2: the slowest dim, possibly in a neighbour's block)
+              const lope_i64 yimg = (yg < g.hi[1] ? (lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdl : 0)
+                                                  : -(lope_i64)g.m[1] * s1 + (Body::RANK == 2 ? g.sdh : 0));
+              if (yw) {
+                *reinterpret_cast<V*>(p + yimg) = o;
+                if (xw) *reinterpret_cast<V*>(p + yimg + ximg) = o;
+              }
+              if (zw) {
+                *reinterpret_cast<V*>(p + zimg) = o;
+                if (xw) *reinterpret_cast<V*>(p + zimg + ximg) = o;
+                if (yw) {
+                  *reinterpret_cast<V*>(p + zimg + yimg) = o;
+                  if (xw) *reinterpret_cast<V*>(p + zimg + yimg + ximg) = o;
+                }
+              }
+            }
+          }
         }
       }
+    };
+    if constexpr (YS) {
+      for (int pz = 0; pz < nz; ++pz) {
+        const int yb_ = ybase + pz * C::BY;
+        const int nr_ = min(RY, g.ext[1] - yb_);
+        const bool wya = (g.wrap & 2) && (nr_ > 0) &&
+                         (lope_near(yb_ + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                          lope_near(yb_ + nr_ - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
+        plane(pz, orow + (lope_i64)pz * C::BY * s1, yb_, nr_, wya);
+      }
+    } else {
+      for (int pz = 0; pz < nz; ++pz, orow += s2) plane(pz, orow, ybase, nrow, wy_any);
     }
     lbase += nz + NZW - 1;
-    // the next unit's window starts NZW - 1 planes further (this unit's trailing halo)
-#pragma unroll
-    for (int k = 0; k < NZW - 1; ++k)
-      if (++c_slot == NS) { c_slot = 0; c_par ^= 1u; }
   }
 }
+
+
 
 // --------------------------------------------------------------------------
 // Temporal blocking (rank 2, one array, every dim periodic): TT fused steps per

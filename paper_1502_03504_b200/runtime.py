@@ -633,6 +633,59 @@ def run_pinned(kernel: CompiledKernel, shape, lo, hi, dtype, host_in, host_out, 
     (stream or _torch().cuda.current_stream()).synchronize()
 
 
+def run_pinned_batch(kernel: CompiledKernel, shape, lo, hi, dtype, host_ins, host_outs, steps: int,
+                     scalars=None, slots: int = 3) -> None:
+    """``run_pinned`` over a sequence of independent fields with the PCIe copies hidden
+    behind the stencil work: field i is uploaded on a copy stream while field i-1 iterates
+    on the compute stream and field i-2 downloads on a third stream (H2D and D2H run in
+    both PCIe directions at once).  ``slots`` device blocks rotate; an upload waits until
+    its slot's previous field has been downloaded.  ``host_ins`` / ``host_outs``: pinned
+    torch CPU tensors (column-major interiors), one per field (the same tensor may repeat).
+    Returns after the last download has completed."""
+    torch = _torch()
+    n = len(host_ins)
+    if len(host_outs) != n:
+        raise ValueError("one output buffer per input field")
+    if n == 0:
+        return
+    cur = torch.cuda.current_stream()
+    h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    for st in (h2d, comp, d2h):
+        st.wait_stream(cur)
+    nslot = max(1, min(slots, n))
+    L = _lib.make_layout(len(shape), dtype, tuple(shape), tuple(lo), tuple(hi))
+    per_slot = 2 * L.count * L.elem_bytes        # one ping-pong pair
+    free_b, _ = torch.cuda.mem_get_info()
+    nslot = max(1, min(nslot, int(0.9 * free_b) // max(1, per_slot)))
+    blocks = []
+    with torch.cuda.stream(comp):
+        for _ in range(nslot):
+            b = HaloArray(shape, lo, hi, dtype)
+            b.spare()               # both ping-pong buffers, zero-filled on `comp`
+            blocks.append(b)
+    h2d.wait_stream(comp)
+    free = [None] * nslot           # event: the slot's last download has been issued/done
+    for i in range(n):
+        k = i % nslot
+        b = blocks[k]
+        if free[k] is not None:
+            h2d.wait_event(free[k])
+        b.upload(host_ins[i].data_ptr(), h2d)
+        up = torch.cuda.Event()
+        up.record(h2d)
+        comp.wait_event(up)
+        iterate(kernel, b, steps, scalars, comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        d2h.wait_event(done)
+        b.download(host_outs[i].data_ptr(), d2h)
+        fr = torch.cuda.Event()
+        fr.record(d2h)
+        free[k] = fr
+    d2h.synchronize()               # every download (and so every iteration) has completed
+    cur.wait_stream(d2h)
+
+
 class StepGraph:
     """``steps`` fused steps captured once as a CUDA graph and replayed.
 

@@ -503,3 +503,24 @@ def test_run_pinned_on_a_side_stream_with_the_default_stream_busy():
         want = O.periodic_apply(want, kir, None, np.float32)
     assert O.equal_bits(got, want)
     torch.cuda.synchronize()
+
+
+def test_run_pinned_batch_matches_single_runs():
+    """run_pinned_batch (uploads, iterations and downloads of independent fields on three
+    streams, device slots reused) gives every field the bits run_pinned gives it."""
+    kir = stencils.lap3d7()
+    k = K(kir, "float32")
+    shape, lo, hi = (136, 40, 23), (1, 1, 1), (1, 1, 1)
+    fields = [np.asfortranarray(O.hash_field(shape, 300 + i, np.float32)) for i in range(5)]
+    ins = [torch.from_numpy(f.ravel(order="F").copy()).pin_memory() for f in fields]
+    outs = [torch.empty_like(t).pin_memory() for t in ins]
+    R.run_pinned_batch(k, shape, lo, hi, "float32", ins, outs, 4, slots=3)
+    for i, t in enumerate(ins):
+        ref = torch.empty_like(t).pin_memory()
+        R.run_pinned(k, shape, lo, hi, "float32", t, ref, 4)
+        assert torch.equal(outs[i].view(torch.int32), ref.view(torch.int32)), i
+        want = fields[i]
+        for _ in range(4):
+            want = O.periodic_apply(want, kir, None, np.float32)
+        got = outs[i].numpy().reshape(shape, order="F")
+        assert O.equal_bits(got, want), i
