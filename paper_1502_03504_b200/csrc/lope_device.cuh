@@ -1091,6 +1091,20 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
             for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
             *reinterpret_cast<V*>(orow + (lope_i64)r * s1) = o;
           }
+        } else if (!(wy_any | zw)) {
+          // x-edge tiles off the y/z boundary: masked vectors and their x images
+          LopeVecOut<T, Body::RANK> vo;
+          vo.init(x, xok, g);
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            vo.put(orow + (lope_i64)r * s1, o);
+            if (vo.xw) vo.putx(orow + (lope_i64)r * s1, o, g);
+          }
         } else {
           LopeVecOut<T, Body::RANK> vo;
           vo.init(x, xok, g);
