@@ -665,7 +665,9 @@ def e2e_measure(args, wl, kern, lo, hi, shape, gshape, esz, group, ws, rank, dev
               "iters_per_call": E2E_ITERS, "calls": reps, "seconds": round(el, 4),
               "api": "runtime.run_pinned (HaloArray upload, iterate, gather)",
               "input": "hash field slab in pinned host memory (column-major)"}
-    if ws > 1 or args.e2e_fields <= 1:
+    if ws > 1 or args.e2e_fields <= 1 or nbytes < (256 << 20):
+        # small fields (config 1: 4 MB) are bound by per-call host work, which a batch
+        # of streams and events only adds to: single calls are the end-to-end number
         return single
     # a batch of independent fields through runtime.run_pinned_batch: field i+1 uploads
     # and field i-1 downloads while field i iterates (3 device slots, 3 streams)

@@ -986,7 +986,11 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
     long long nty = (ext[1] + c.wy * c.ry - 1) / (c.wy * c.ry);
     long long nzc = (ext[2] + g.zchunk - 1) / g.zchunk;
     if (k.rank == 2) {
-      // rank 2 streams units along y: `zchunk` y tiles per unit (lope_tiled_impl, YS)
+      // rank 2 streams units along y: `zchunk` y tiles per unit (lope_tiled_impl, YS);
+      // small fields keep at least two units per resident CTA (1024^2 has only 256
+      // tiles: 8-tile units would leave most SMs idle)
+      const long long cap = 2LL * m->tiled_blocks * sm_count();
+      while (g.zchunk > 1 && ntx * ((nty + g.zchunk - 1) / g.zchunk) < cap) g.zchunk = (g.zchunk + 1) / 2;
       nty = (nty + g.zchunk - 1) / g.zchunk;
       nzc = 1;
     }
