@@ -1179,6 +1179,9 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
         plane(pz, orow + (lope_i64)pz * C::BY * s1, yb_, nr_, wya);
       }
     } else {
+#ifdef LOPE_UNROLL2
+#pragma unroll 2
+#endif
       for (int pz = 0; pz < nz; ++pz, orow += s2) plane(pz, orow, ybase, nrow, wy_any);
     }
     lbase += nz + NZW - 1;
