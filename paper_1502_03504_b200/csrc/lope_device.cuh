@@ -1555,10 +1555,19 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
     const int x = w.tx * C::BX + cx;
     const int ybase = w.ty() * C::BY + row0;
     const bool xok = x < g.ext[0];
-    LopeVecOut<T, Body::RANK> vo;
-    vo.init(x, xok, g);
     const int nrow = min(RY, g.ext[1] - ybase);
     const lope_i64 rowoff = x + (lope_i64)ybase * s1 + (lope_i64)z0 * s2;
+    // warp-uniform: whole in-range vectors, no x image, no y image -> plain stores (the
+    // masked / image store state is rebuilt only where it is needed: register pressure)
+    bool plain;
+    {
+      LopeVecOut<T, Body::RANK> v0;
+      v0.init(x, xok, g);
+      const bool wy = (g.wrap & 2) && nrow > 0 &&
+                      (lope_near(ybase + g.r0[1], g.m[1], g.lo[1], g.hi[1]) ||
+                       lope_near(ybase + nrow - 1 + g.r0[1], g.m[1], g.lo[1], g.hi[1]));
+      plain = __all_sync(0xffffffffu, !wy && !v0.xw && (!xok || v0.xm == v0.ALL));
+    }
     for (int pz = 0; pz < nz; ++pz) {
       if (!PW && warp == 0) {
         if (lane == 0) produce(lbase + pz + NS);
@@ -1632,21 +1641,39 @@ __device__ __forceinline__ void lope_tiled_multi_impl(const LopeTmapPack<Body::N
       // the periodic images the next HALO_TRANSFER would write
       const int zg = z0 + pz + g.r0[2];
       const bool zw = (g.wrap & 4) && lope_near(zg, g.m[2], g.lo[2], g.hi[2]);
-      const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
+      if (plain && !zw) {
 #pragma unroll
-      for (int q = 0; q < Body::NSTORE; ++q) {
-        T* ob = arrs.a[Body::stored(q)].out + arrs.a[Body::stored(q)].org + rowoff + (lope_i64)pz * s2;
+        for (int q = 0; q < Body::NSTORE; ++q) {
+          T* ob = arrs.a[Body::stored(q)].out + arrs.a[Body::stored(q)].org + rowoff + (lope_i64)pz * s2;
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-          if (r >= nrow) continue;
-          V o;
-          T* oe = reinterpret_cast<T*>(&o);
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
 #pragma unroll
-          for (int e = 0; e < VX; ++e) oe[e] = vals[r][e][q];
-          if (g.wrap)
-            vo.store_all(ob + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
-          else
-            vo.put(ob + (lope_i64)r * s1, o);
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e][q];
+            *reinterpret_cast<V*>(ob + (lope_i64)r * s1) = o;
+          }
+        }
+      } else {
+        LopeVecOut<T, Body::RANK> vo;
+        vo.init(x, xok, g);
+        const lope_i64 zimg = (zg < g.hi[2] ? (lope_i64)g.m[2] * s2 + g.sdl : -(lope_i64)g.m[2] * s2 + g.sdh);
+#pragma unroll
+        for (int q = 0; q < Body::NSTORE; ++q) {
+          T* ob = arrs.a[Body::stored(q)].out + arrs.a[Body::stored(q)].org + rowoff + (lope_i64)pz * s2;
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (r >= nrow) continue;
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e][q];
+            if (g.wrap)
+              vo.store_all(ob + (lope_i64)r * s1, o, ybase + r + g.r0[1], zw, zimg, s1, g);
+            else
+              vo.put(ob + (lope_i64)r * s1, o);
+          }
         }
       }
     }
