@@ -204,6 +204,35 @@ def test_boundary_rejects_bad_calls_with_reference_codes():
     _lib.destroy_kernel(h)
 
 
+def test_step_arrays_rejects_bad_calls_with_reference_codes():
+    """lope_step_arrays (fused steps of multi-array kernels) checks its arguments before
+    any device work: aliasing outputs and layout mismatches are E108, a footprint wider
+    than an array's halo E102, a missing buffer E202."""
+    import ctypes
+    L = _lib.lib()
+    kb = KernelBuilder("two", 2)
+    u, v = kb.array("u"), kb.array("v")
+    kb.store(u, u[0, 0] + 0.5 * (v[1, 0] + v[0, -1]))
+    h = _lib.compile_kernel(serialize(kb.build()), "f32")
+    lay = _lib.make_layout(2, "f32", (64, 32), (1, 1), (1, 1))
+    other = _lib.make_layout(2, "f32", (64, 16), (1, 1), (1, 1))
+    thin = _lib.make_layout(2, "f32", (64, 32), (0, 0), (0, 1))
+    rs, is_ = (ctypes.c_double * 1)(), (ctypes.c_int64 * 1)()
+    A, B, C = 0x1000, 0x2000, 0x3000
+
+    def call(layouts, ins, outs):
+        lays = (_lib.Layout * 2)(*layouts)
+        return L.lope_step_arrays(h, lays, (ctypes.c_void_p * 2)(*ins), (ctypes.c_void_p * 2)(*outs),
+                                  rs, is_, 3, None)
+
+    assert call((lay, lay), (A, B), (A, None)) == 108          # u's output aliases its snapshot
+    assert call((lay, other), (A, B), (C, None)) == 108        # different interiors
+    assert call((lay, thin), (A, B), (C, None)) == 102         # v read at x+1 / y-1, halo (0,0)/(0,1)
+    assert call((lay, lay), (A, None), (C, None)) == 202       # v not allocated
+    assert call((lay, lay), (A, B), (None, None)) == 202       # stored u has no output
+    _lib.destroy_kernel(h)
+
+
 def test_comm_boundary_checks_without_a_gpu():
     """lope_comm's argument and setup-order checks (no device work): the reference's
     E-codes for a bad image index (E201) and missing setup (E202)."""
