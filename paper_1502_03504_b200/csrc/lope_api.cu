@@ -1533,13 +1533,6 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       t.wy = 8;
       t.ry = 4;
       for (int zc : {32, 64}) c.push_back({t, zc, 0});
-      // 16 warps x 4 rows (64-row tiles, 36 KB stages, 6-deep ring): the same per-point
-      // overhead with twice the warps in flight and half the y-halo re-reads
-      TileCfg t6 = base;
-      t6.ry = 4;
-      t6.ns = 6;
-      if (tiled_smem_bytes(K->ir, K->dtype, t6) <= 225 * 1024)
-        for (int zc : {32, 64}) c.push_back({t6, zc, 0});
       t.pw = 1;
       t.ns = 12;
       t.sh = 1;
