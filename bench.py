@@ -533,7 +533,7 @@ def run_gpu_arm(args, wl):
     if ws == 1:
         traffic, traffic_src = ncu_traffic(args.workload, plan)
     else:       # the captures are of the one-GPU workload; a slab's geometry differs
-        traffic, traffic_src = None, "no capture of the N>1 slab geometry
+        traffic, traffic_src = None, "no capture of the N>1 slab geometry"
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
