@@ -194,6 +194,7 @@ def _multi_kernel(rank, na):
 @pytest.mark.parametrize("rank,na,dt,shape", [
     (2, 2, "float32", (136, 45)), (2, 3, "float64", (70, 33)), (3, 2, "float32", (72, 21, 13)),
     (3, 2, "float64", (37, 18, 11)), (2, 4, "float32", (129, 40)), (2, 2, "float32", (10, 9)),
+    (3, 3, "float32", (131, 17, 9)), (2, 2, "float64", (301, 27)),
 ])
 def test_multi_array_fused_steps_match_the_oracle(rank, na, dt, shape):
     """iterate_arrays: fused steps on the multi-array TMA kernel (images of every stored
@@ -222,3 +223,56 @@ def test_multi_array_fused_steps_match_the_oracle(rank, na, dt, shape):
         assert O.equal_bits(got, bufs[p]), (p, O.first_mismatch(got, bufs[p]))
     n = launches(k)
     assert n["tiled_multi"] == steps and n["generic"] == 0, n
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_multi_array_unaligned_subranges_match_the_oracle(dt):
+    """Plain launches of a multi-array kernel over sub-ranges whose x start and end fall
+    inside a vector, on an odd-width interior: the multi-array TMA kernel masks its edge
+    vectors; cells outside the range keep their snapshots (copy-through)."""
+    kir = _multi_kernel(3, 2)
+    k = R.CompiledKernel(kir, dt)
+    shape = (75, 19, 11)
+    lo, hi = [1] * 3, [1] * 3
+    rng = np.random.default_rng(31)
+    fields = [O.hash_field(shape, 120 + i, NP[dt]) for i in range(2)]
+    for _ in range(5):
+        ranges = []
+        for m in shape:
+            a = int(rng.integers(1, m // 2))
+            b = int(rng.integers(a, m + 1))
+            ranges.append((a, b))
+        hs = []
+        for f in fields:
+            h = R.HaloArray(shape, lo, hi, dt)
+            h.set_interior(f)
+            R.halo_transfer(h)
+            hs.append(h)
+        R.launch(k, hs, ranges)
+        bufs = {p: O.embed(f, lo, hi, NP[dt]) for p, f in zip(kir.array_params, fields)}
+        for b in bufs.values():
+            O.halo_fill(b, lo, hi)
+        O.launch(bufs, {p: (lo, hi) for p in kir.array_params}, kir, ranges, None, NP[dt])
+        for p, h in zip(kir.array_params, hs):
+            got = h.get_padded()
+            assert O.equal_bits(got, bufs[p]), (p, ranges, O.first_mismatch(got, bufs[p]))
+    n = launches(k)
+    assert n["tiled_multi"] == 5 and n["generic"] == 0, n
+
+
+def test_run_pinned_batch_fp64_rank2_ragged():
+    """The pipelined batch on a ragged rank-2 fp64 field (RAG tiled kernel) equals single
+    runs field by field."""
+    kir = stencils.box5x5()
+    k = R.CompiledKernel(kir, "float64")
+    shape, lo, hi = (203, 77), (2, 2), (2, 2)
+    fields = [np.asfortranarray(O.hash_field(shape, 500 + i, np.float64)) for i in range(4)]
+    ins = [torch.from_numpy(f.ravel(order="F").copy()).pin_memory() for f in fields]
+    outs = [torch.empty_like(t).pin_memory() for t in ins]
+    R.run_pinned_batch(k, shape, lo, hi, "float64", ins, outs, 3, slots=2)
+    for i, f in enumerate(fields):
+        want = f
+        for _ in range(3):
+            want = O.periodic_apply(want, kir, None, np.float64)
+        got = outs[i].numpy().reshape(shape, order="F")
+        assert O.equal_bits(got, want), i
