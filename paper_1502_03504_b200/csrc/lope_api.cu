@@ -1511,32 +1511,30 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
   std::vector<PlanCand> c;
   const TileCfg base = K->variants[0].tile;
   if (K->ir.rank == 3) {
-    for (int zc : {16, 32, 64}) c.push_back({base, zc, 0});
+    // the plans that won on B200 across configs 3 and 5 and the random-kernel sweeps
+    // (profiles/r02: 16-plane chunks, 3-4-plane chunks and 16 warps x 4 rows never did);
+    // ten candidates keep tuning at ~130 steps
+    for (int zc : {32, 64}) c.push_back({base, zc, 0});
     if (base.pw == 0) {
       // in-band producer that only prefetches into free slots (2048^3: 13.4 vs 14.4 ms;
       // 1024^3: 1.57 vs 1.51 ms -- hence a candidate, not the default)
       TileCfg t = base;
       t.nb = 1;
-      for (int zc : {32, 64}) c.push_back({t, zc, 0});
+      c.push_back({t, 64, 0});
     }
     for (int ns : {8, 10, 12}) {
       TileCfg t = base;
       t.pw = 1;
       t.ns = ns;
       t.sh = 1;
-      // (y-banded walks, yband 4-16, measured no better on 1024^3 / 2048^3)
-      for (int zc : {3, 4, 6, 8}) c.push_back({t, zc, 0});
+      for (int zc : {6, 8}) c.push_back({t, zc, 0});
     }
     if (K->dtype == LOPE_F32) {
       // 8 warps x 4 rows per lane: half the per-plane overhead per point
       TileCfg t = base;
       t.wy = 8;
       t.ry = 4;
-      for (int zc : {32, 64}) c.push_back({t, zc, 0});
-      t.pw = 1;
-      t.ns = 12;
-      t.sh = 1;
-      for (int zc : {3, 4, 6}) c.push_back({t, zc, 0});
+      c.push_back({t, 64, 0});
     }
   } else {
     // 2-D: the dedicated producer always won (ninept2d 16384^2: 0.355 vs 0.50 ms in-band),

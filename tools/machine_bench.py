@@ -62,6 +62,12 @@ def main():
                 torch.cuda.synchronize()
                 out, el = timed_run(lambda: GpuMachine(chk, RunConfig(steps=a.steps, **cfg), field.copy(),
                                                         dtype=dt))
+                # marginal cost of a step: the same run with 5x the steps (the one-time host
+                # scatter of the input field in lopec's own _alloc_host, uploads and the final
+                # gather cancel out)
+                _, el5 = timed_run(lambda: GpuMachine(chk, RunConfig(steps=5 * a.steps, **cfg), field.copy(),
+                                                       dtype=dt))
+                step_ms = 1e3 * (el5 - el) / (4 * a.steps)
                 chk_bits = None
                 if dt == "float64":
                     g_out, _ = timed_run(lambda: GpuMachine(chk, RunConfig(steps=a.ref_steps, **cfg), field.copy(),
@@ -71,6 +77,8 @@ def main():
                     "program": kernel, "shape": list(shape), "images": images, "grid_rows": cfg["grid_rows"],
                     "dtype": dt, "steps": a.steps, "gpu_machine_s": round(el, 4),
                     "gpu_machine_gpts": round(pts * a.steps / el / 1e9, 3),
+                    "gpu_machine_marginal_ms_per_step": round(step_ms, 4),
+                    "gpu_machine_marginal_gpts": round(pts / (step_ms * 1e-3) / 1e9, 2) if step_ms > 0 else None,
                     "reference_machine_steps": a.ref_steps, "reference_machine_s": round(ref_s, 3),
                     "reference_machine_gpts": round(pts * a.ref_steps / ref_s / 1e9, 4),
                     "bitwise_equal_to_reference_fp64": chk_bits,
