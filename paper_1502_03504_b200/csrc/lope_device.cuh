@@ -375,60 +375,8 @@ __device__ __forceinline__ void lope_mbar_expect_tx(lope_u64* bar, lope_u32 byte
 #if !defined(LOPE_WAIT_HINT_NS) && !defined(LOPE_NO_WAIT_HINT)
 #define LOPE_WAIT_HINT_NS 5000
 #endif
-// Shared-window address of a barrier (computed once per kernel; the generic-to-shared
-// conversion costs an S2R + LEA when left inside the plane loop).
-__device__ __forceinline__ bool lope_mbar_test_addr(lope_u32 addr, lope_u32 parity) {
-  lope_u32 done = 0;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n}"
-      : "=r"(done)
-      : "r"(addr), "r"(parity)
-      : "memory");
-  return done != 0;
-}
-__device__ __forceinline__ void lope_mbar_wait_slow(lope_u32 addr, lope_u32 parity);
-// Fast path: one non-blocking probe (the phase has usually completed -- the producer
-// runs NS-HOLD planes ahead); only a miss enters the suspending, bounded wait loop.
-__device__ __forceinline__ void lope_mbar_wait_addr(lope_u32 addr, lope_u32 parity) {
-#ifdef LOPE_NO_PROBE
-  lope_mbar_wait_slow(addr, parity);
-#else
-  if (!lope_mbar_test_addr(addr, parity)) lope_mbar_wait_slow(addr, parity);
-#endif
-}
-__device__ __forceinline__ void lope_mbar_arrive_addr(lope_u32 addr) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
-}
 __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
   const lope_u32 addr = lope_smem_u32(bar);
-  lope_u32 done = 0, n = 0;
-  do {
-#ifdef LOPE_WAIT_HINT_NS
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity), "n"(LOPE_WAIT_HINT_NS)
-        : "memory");
-#else
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-#endif
-    if (++n > LOPE_WAIT_LIMIT) __trap();
-  } while (!done);
-}
-// The bounded, suspending loop of lope_mbar_wait_addr: a TMA that never lands traps
-// (kernel error) instead of hanging the GPU.  (Inline: a call would make the compiler
-// save the live register window to local memory around it.)
-__device__ __forceinline__ void lope_mbar_wait_slow(lope_u32 addr, lope_u32 parity) {
   lope_u32 done = 0, n = 0;
   do {
 #ifdef LOPE_WAIT_HINT_NS
