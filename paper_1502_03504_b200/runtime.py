@@ -656,6 +656,8 @@ def run_pinned_batch(kernel: CompiledKernel, shape, lo, hi, dtype, host_ins, hos
     L = _lib.make_layout(len(shape), dtype, tuple(shape), tuple(lo), tuple(hi))
     per_slot = 2 * L.count * L.elem_bytes        # one ping-pong pair
     free_b, _ = torch.cuda.mem_get_info()
+    # blocks torch's caching allocator holds but does not use count as free too
+    free_b += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     nslot = max(1, min(nslot, int(0.9 * free_b) // max(1, per_slot)))
     blocks = []
     with torch.cuda.stream(comp):

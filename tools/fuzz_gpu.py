@@ -1,11 +1,13 @@
 """GPU fuzz: random locally-oriented kernels through the product path vs the oracle.
 
 Random IR trees (+ - * / with constant, scalar and expression divisors, abs, sqrt,
-min, max, locals, pending-centre reads, one or two arrays), random rank 2/3, halos at
+min, max, locals, pending-centre reads, one or two arrays), random rank 1/2/3, halos at
 least the footprint (sometimes wider, asymmetric), ragged or vector-aligned shapes,
-fp32 and fp64; ``iterate`` for a few steps (tiled or generic path, fused halo images,
-temporal blocking for small 2-D fields) compared bit for bit with the numpy
-restatement (fp64 == the reference's arithmetic).  Exits non-zero on a mismatch.
+fp32 and fp64; ``iterate`` (one array) or ``iterate_arrays`` / per-step launches (two
+arrays) for a few steps (tiled, RAG, row, multi-array or temporal-blocking kernels,
+fused halo images) compared bit for bit with the numpy restatement (fp64 == the
+reference's arithmetic).  Prints the launches per kernel family.  Exits non-zero on a
+mismatch.
 
     python tools/fuzz_gpu.py [cases] [seed] [--decomp]
 
@@ -71,8 +73,11 @@ def make_kernel(rng, rank):
     return kb.build()
 
 
+PATHS = {}
+
+
 def run_case(rng, case):
-    rank = 2 if rng.random() < 0.6 else 3
+    rank = rng.choice([1, 2, 2, 2, 3, 3])
     try:
         kir = make_kernel(rng, rank)
     except ValueError:          # E103-style programs the checker rejects
@@ -83,11 +88,14 @@ def run_case(rng, case):
     fps = [kir.footprints[a].dims for a in kir.array_params]
     lo = [max(f[d][0] for f in fps) + (rng.randrange(2) if rng.random() < 0.3 else 0) for d in range(rank)]
     hi = [max(f[d][1] for f in fps) + (rng.randrange(2) if rng.random() < 0.3 else 0) for d in range(rank)]
-    if rank == 2:
+    if rank == 1:
+        shape = (rng.choice([rng.randrange(max(lo[0] + hi[0], 2), 64), rng.randrange(64, 5000)]),)
+    elif rank == 2:
         mx = rng.choice([rng.randrange(9, 90) * vx, rng.randrange(20, 300), 288, 320])
         shape = (mx, rng.randrange(max(lo[1] + hi[1], 5), 80))
     else:
-        shape = (rng.randrange(9, 40) * vx, rng.randrange(max(lo[1] + hi[1], 4), 30),
+        mx = rng.choice([rng.randrange(9, 40) * vx, rng.randrange(5, 160)])     # ragged x too
+        shape = (mx, rng.randrange(max(lo[1] + hi[1], 4), 30),
                  rng.randrange(max(lo[2] + hi[2], 3), 20))
     if any(s < l + h or s < 1 for s, l, h in zip(shape, lo, hi)):
         return None
@@ -109,17 +117,25 @@ def run_case(rng, case):
                 want = np.broadcast_to(O.periodic_apply(want, kir, sc, npdt), shape).astype(npdt)
         want = [want]
     else:
-        # two arrays: one launch per step after a periodic halo fill of both (the oracle
-        # works on the dense periodic fields)
+        # two arrays: either one launch per step after a periodic halo fill of both, or
+        # iterate_arrays (fused steps storing every stored array's images); the oracle
+        # works on the dense periodic fields
         cur = list(fields)
+        if rng.random() < 0.5:
+            R.iterate_arrays(k, arrs, steps, sc)
+        else:
+            for _ in range(steps):
+                for a in arrs:
+                    R.halo_transfer(a)
+                R.launch(k, arrs, None, sc)
         for _ in range(steps):
-            for a in arrs:
-                R.halo_transfer(a)
-            R.launch(k, arrs, None, sc)
             with np.errstate(all="ignore"):
                 cur = _oracle_multi(kir, cur, sc, npdt)
         got = [a.get_interior() for a in arrs]
         want = cur
+    import json as _json
+    for fam, n in _json.loads(k.describe())["launches"].items():
+        PATHS[fam] = PATHS.get(fam, 0) + n
     for g_, w_ in zip(got, want):
         if not O.equal_bits(g_, w_):
             return (kir, dt, shape, lo, hi, steps, O.first_mismatch(g_, w_))
@@ -208,6 +224,8 @@ def main():
             kir, dt, shape, lo, hi, steps, mm = r
             print("MISMATCH", dt, shape, lo, hi, steps, mm, kir, flush=True)
     print(f"fuzz: {ran} cases, {bad} mismatches", flush=True)
+    if PATHS:
+        print("launches per kernel family:", PATHS, flush=True)
     sys.exit(1 if bad else 0)
 
 
