@@ -571,6 +571,10 @@ def run_gpu_arm(args, wl):
                      "frac_of_measured_peak_median": round(2 * esz * points / (med / 1e3) / 1e9 / measured_peak()[0], 4),
                      "clocks": sclk.summary(),
                      "note": "per-rank device time of rank 0" if ws > 1 else "device time, CUDA events per step"}
+        pw = (sustained["clocks"] or {}).get("power_w_median")
+        if pw:
+            # board energy per billion point updates at the capped steady state
+            sustained["joules_per_gpoint"] = round(pw / (points / (med / 1e3) / 1e9), 4)
 
     # the device-timed blocks are done: free them before the e2e batch allocates its
     # own (config 5: 69 GB per ping-pong pair; with them alive only one batch slot fits)

@@ -449,7 +449,8 @@ template <> struct LopeVec<double> { typedef double2 V; };
 
 // --------------------------------------------------------------------------
 // One lane's 16-byte output vector and the periodic images the fused epilogue owes
-// (shared by the tiled kernels).  x runs from the launch range's start rounded down
+// (the HALO_TRANSFER fills of runtime.py:653-697 with neighbour == self; shared by the
+// RAG tiled instantiation and the multi-array kernel).  x runs from the launch range's start rounded down
 // to a whole vector: the first g.xshift cells and the cells past g.ext[0] are outside
 // the range (ragged starts / extents store element by element).  When images are
 // refreshed m[d] >= lo[d] + hi[d] (each halo cell has exactly one image); x images
@@ -523,7 +524,8 @@ struct LopeVecOut {
 };
 
 // --------------------------------------------------------------------------
-// Rank-1 path (any number of arrays): each thread owns one 16-byte vector of every
+// Rank-1 path (Machine._launch_vector, runtime.py:605-618, for rank-1 kernels such as
+// corpus/avg3.lope; any number of arrays): each thread owns one 16-byte vector of every
 // array (coalesced LDG.128 through the read-only path) and reads the x halo of its
 // points with scalar loads that hit L1 (the neighbouring lanes' lines).  x runs from
 // the range start rounded down to a whole vector; cells outside the launch range are

@@ -522,7 +522,8 @@ def step_arrays(kernel: CompiledKernel, arrays: Sequence[HaloArray], scalars=Non
                 wrap_mask: Optional[int] = None, stream=None) -> None:
     """``step`` for kernels over several arrays: one fused full-interior launch whose
     stored arrays also receive their periodic images (``lope_step_arrays``) -- the state
-    after the launch and the next ``HALO_TRANSFER`` of every stored array."""
+    after the launch (runtime.py:541-618) and the next ``HALO_TRANSFER`` of every stored
+    array (runtime.py:643-697)."""
     ir = kernel.ir
     if len(arrays) != len(ir.array_params):
         raise RuntimeFault(ALLOC_SHAPE, f"kernel '{ir.name}' takes {len(ir.array_params)} arrays")
