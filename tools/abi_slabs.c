@@ -139,6 +139,10 @@ static int mode_rr(int P, int64_t n, int steps) {
   CUCHECK(cudaMemset(ga, 0, G.count * 4));
   CUCHECK(cudaMemset(gb, 0, G.count * 4));
   CHECK(lope_fill_hash(&G, ga, 20260823ULL, gext, gorg, 0));
+  cudaEvent_t g0, g1;
+  CUCHECK(cudaEventCreate(&g0));
+  CUCHECK(cudaEventCreate(&g1));
+  CUCHECK(cudaEventRecord(g0, 0));
   CHECK(lope_halo_fill(&G, ga, 7, 0));
   for (int s = 0; s < steps - 1; ++s) {
     CHECK(lope_step(k, &G, ga, gb, NULL, NULL, 7, 0));
@@ -148,7 +152,10 @@ static int mode_rr(int P, int64_t n, int steps) {
   const void* in[1] = {ga};
   void* out[1] = {gb};
   CHECK(lope_launch(k, &G, rng, in, out, NULL, NULL, 0));
+  CUCHECK(cudaEventRecord(g1, 0));
   CUCHECK(cudaDeviceSynchronize());
+  float ms_single = 0;
+  CUCHECK(cudaEventElapsedTime(&ms_single, g0, g1));
   /* compare interiors */
   const size_t slab = (size_t)n * n * n;
   float* hs = (float*)malloc(slab * 4);
@@ -170,9 +177,10 @@ static int mode_rr(int P, int64_t n, int steps) {
   }
   double pts = (double)n * n * n * P;
   printf("{\"mode\": \"rr\", \"images\": %d, \"slab\": [%lld, %lld, %lld], \"steps\": %d, \"ms_total\": %.3f, "
-         "\"gpts\": %.2f, \"bitwise_equal_to_undecomposed\": %s, \"err\": \"%s\"}\n",
-         P, (long long)n, (long long)n, (long long)n, steps, ms, pts * steps / (ms / 1e3) / 1e9,
-         bad ? "false" : "true", cudaGetErrorString(cudaGetLastError()));
+         "\"gpts\": %.2f, \"ms_total_undecomposed\": %.3f, \"gpts_undecomposed\": %.2f, "
+         "\"bitwise_equal_to_undecomposed\": %s, \"err\": \"%s\"}\n",
+         P, (long long)n, (long long)n, (long long)n, steps, ms, pts * steps / (ms / 1e3) / 1e9, ms_single,
+         pts * steps / (ms_single / 1e3) / 1e9, bad ? "false" : "true", cudaGetErrorString(cudaGetLastError()));
   for (int r = 0; r < P; ++r) lope_comm_destroy(im[r].comm);
   lope_kernel_destroy(k);
   return bad ? 2 : 0;
