@@ -883,12 +883,34 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
       }
       // ---- wait for the planes this iteration reads ----
       const T* sp[NZW];
+#ifdef LOPE_SLOT_INC
+      // one division per plane: the window's slots follow the first one
+      const lope_u32 L0 = lbase + pz;
+      const lope_u32 s0 = L0 % NS, q0 = L0 / NS;
+#endif
 #pragma unroll
       for (int k = 0; k < NZW; ++k) {
         const lope_u32 L = lbase + pz + k;
+#ifdef LOPE_SLOT_INC
+        const lope_u32 sl = s0 + k >= (lope_u32)NS ? s0 + k - NS : s0 + k;
+        const lope_u32 ph = (s0 + k >= (lope_u32)NS ? q0 + 1 : q0) & 1;
+        sp[k] = reinterpret_cast<const T*>(lope_smem + sl * C::STAGE_BYTES) + soff;
+#else
         sp[k] = reinterpret_cast<const T*>(lope_smem + (L % NS) * C::STAGE_BYTES) + soff;
+#endif
+#ifdef LOPE_SLIDE_WAIT
+        // after the unit's first plane only the newest plane is new: the others were
+        // waited for by an earlier plane and a slot is not refilled while this warp holds it
+        if (pz > 0 && k < NZW - 1) continue;
+#else
         if (ZHIST && k < FZN && pz > 0) continue;          // past planes come from registers
+#endif
+#ifdef LOPE_SLOT_INC
+        (void)L;
+        lope_mbar_wait(&full[sl], ph);
+#else
         lope_mbar_wait(&full[L % NS], (L / NS) & 1);
+#endif
       }
       if (ZHIST && pz == 0) {
         // history for the first plane of the unit: planes z0-1 .. z0-FZN at own points
