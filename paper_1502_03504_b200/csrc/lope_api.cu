@@ -1513,8 +1513,9 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
   if (K->ir.rank == 3) {
     // the plans that won on B200 across configs 3 and 5 and the random-kernel sweeps
     // (profiles/r02: 16-plane chunks, 3-4-plane chunks and 16 warps x 4 rows never did);
-    // ten candidates keep tuning at ~130 steps
-    for (int zc : {32, 64}) c.push_back({base, zc, 0});
+    // nine candidates keep tuning at ~120 steps; the in-band plan keeps 64-plane chunks
+    // only (the watchdog's fallback: 32-plane chunks ran 1.58 vs 1.50 ms on config 3)
+    c.push_back({base, 64, 0});
     if (base.pw == 0) {
       // in-band producer that only prefetches into free slots (2048^3: 13.4 vs 14.4 ms;
       // 1024^3: 1.57 vs 1.51 ms -- hence a candidate, not the default)
