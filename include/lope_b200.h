@@ -139,6 +139,14 @@ int lope_unpack_padded(const lope_layout* layout, const void* dev, void* host, v
 int lope_copy_box(const lope_layout* layout, void* dst, const void* src, const int64_t* dst_lo,
                   const int64_t* src_lo, const int64_t* extent, void* stream);
 
+/* n such box copies (all of one layout) in as few launches as possible (up to 32 boxes
+ * per launch): one phase of _halo_exchange (runtime.py:669-711) -- the border pulls, the
+ * neighbour fills or the mirror pushes of every image -- costs one launch instead of one
+ * per image and face.  dst[i] / src[i]: block pointers; dst_lo / src_lo / extent: 3n
+ * entries.  Boxes must not overlap another box's destination.  E108 / E202 as above. */
+int lope_copy_boxes(const lope_layout* layout, int32_t n, void* const* dst, const void* const* src,
+                    const int64_t* dst_lo, const int64_t* src_lo, const int64_t* extent, void* stream);
+
 /* Fill the interior with the synthetic U(-1,1) field: value of global cell
  * g = (o0+i) + G0*((o1+j) + G1*(o2+k)) is splitmix64-hash(g, seed) (oracle/
  * lope_oracle.py: hash_values).  global_extent / global_origin have 3 entries. */

@@ -22,7 +22,7 @@ DTYPES = {"f32": F32, "float32": F32, "f64": F64, "float64": F64}
 EXPORTS = ("lope_abi_version", "lope_last_error", "lope_set_cache_dir", "lope_layout_init",
            "lope_kernel_compile", "lope_kernel_destroy", "lope_kernel_describe",
            "lope_kernel_source", "lope_launch", "lope_step", "lope_step_arrays", "lope_step_planes", "lope_halo_fill", "lope_pack",
-           "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_plan_set_variant", "lope_kernel_prepare", "lope_step_multi",
+           "lope_unpack", "lope_pack_padded", "lope_unpack_padded", "lope_copy_box", "lope_copy_boxes", "lope_box_pack", "lope_plan_candidates", "lope_plan_set", "lope_plan_set_tile", "lope_plan_set_variant", "lope_kernel_prepare", "lope_step_multi",
            "lope_step_planes_peer", "lope_ipc_export", "lope_ipc_open", "lope_ipc_close", "lope_copy_bytes",
            "lope_box_unpack", "lope_fill_hash", "lope_face_span", "lope_launch_count",
            "lope_comm_create", "lope_comm_destroy", "lope_comm_record_size", "lope_comm_export",
@@ -76,6 +76,7 @@ def lib():
     L.lope_pack_padded.argtypes = [P(Layout), VP, VP, VP]
     L.lope_unpack_padded.argtypes = [P(Layout), VP, VP, VP]
     L.lope_copy_box.argtypes = [P(Layout), VP, VP, P(I64), P(I64), P(I64), VP]
+    L.lope_copy_boxes.argtypes = [P(Layout), I32, P(VP), P(VP), P(I64), P(I64), P(I64), VP]
     L.lope_kernel_prepare.argtypes = [VP]
     L.lope_step_planes_peer.argtypes = [VP, P(Layout), VP, VP, I64, I64, P(ctypes.c_double), P(I64), I32, VP, VP, VP]
     L.lope_ipc_export.argtypes = [VP, ctypes.c_char_p, P(I64)]

@@ -251,6 +251,44 @@ __global__ void __launch_bounds__(256) lope_k_copy_box(T* __restrict__ dst, cons
   }
 }
 
+// Several boxes of one layout in one launch (blockIdx.y = box): the halo slabs of one
+// exchange phase.  Rows at least half a warp wide are copied a warp per row (coalesced);
+// thinner boxes (the x-halo columns) a thread per cell, so a 1-cell-wide slab of 4K rows
+// does not leave 31 lanes of every warp idle.
+#define LOPE_MAX_BOXES 32
+template <class T>
+struct LopeBoxes {
+  T* dst[LOPE_MAX_BOXES];
+  const T* src[LOPE_MAX_BOXES];
+  long long d[LOPE_MAX_BOXES][3], s[LOPE_MAX_BOXES][3], e[LOPE_MAX_BOXES][3];
+};
+template <class T>
+__global__ void __launch_bounds__(256) lope_k_copy_boxes(const __grid_constant__ LopeBoxes<T> bx, DevLayout L) {
+  const int b = blockIdx.y;
+  const long long e0 = bx.e[b][0], e1 = bx.e[b][1], e2 = bx.e[b][2];
+  T* dst = bx.dst[b] + L.B + bx.d[b][0] + bx.d[b][1] * L.S1 + bx.d[b][2] * L.S2;
+  const T* src = bx.src[b] + L.B + bx.s[b][0] + bx.s[b][1] * L.S1 + bx.s[b][2] * L.S2;
+  const long long nrows = e1 * e2;
+  if (e0 >= 16) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = warp; r < nrows; r += nw) {
+      const long long j = r % e1, k = r / e1;
+      const long long off = j * L.S1 + k * L.S2;
+      for (long long x = lane; x < e0; x += 32) dst[off + x] = src[off + x];
+    }
+  } else {
+    const long long n = nrows * e0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+      const long long x = i % e0, r = i / e0;
+      const long long j = r % e1, k = r / e1;
+      const long long off = j * L.S1 + k * L.S2 + x;
+      dst[off] = src[off];
+    }
+  }
+}
+
 // Box <-> contiguous buffer (column-major within the box): the strided faces of a
 // decomposed non-slowest dim travel between GPUs through such buffers.
 template <class T, bool PACK>
@@ -1150,6 +1188,40 @@ int run_body(lope_kernel* K, const lope_layout* layouts, const int r0[3], const 
   return 0;
 }
 
+template <class T>
+int copy_boxes_t(const lope_layout* layout, int32_t n, void* const* dst, const void* const* src,
+                 const int64_t* dst_lo, const int64_t* src_lo, const int64_t* extent, cudaStream_t st) {
+  DevLayout d = dev_layout(layout);
+  for (int32_t i0 = 0; i0 < n; i0 += LOPE_MAX_BOXES) {
+    LopeBoxes<T> bx;
+    std::memset(&bx, 0, sizeof bx);
+    int nb = 0;
+    long long most = 1;
+    for (int32_t i = i0; i < n && nb < LOPE_MAX_BOXES; ++i) {
+      const int64_t* e = extent + 3 * i;
+      if (e[0] == 0 || e[1] == 0 || e[2] == 0) continue;      // empty box
+      bx.dst[nb] = (T*)dst[i];
+      bx.src[nb] = (const T*)src[i];
+      for (int k = 0; k < 3; ++k) {
+        bx.d[nb][k] = dst_lo[3 * i + k];
+        bx.s[nb][k] = src_lo[3 * i + k];
+        bx.e[nb][k] = e[k];
+      }
+      const long long work = e[0] >= 16 ? e[1] * e[2] * 32 : e[0] * e[1] * e[2];
+      most = std::max(most, work);
+      ++nb;
+    }
+    if (nb == 0) continue;
+    long long blocks = (most + 255) / 256;
+    const long long cap = std::max<long long>(1, (long long)sm_count() * 16 / nb);
+    if (blocks > cap) blocks = cap;
+    lope_k_copy_boxes<T><<<dim3((unsigned)blocks, (unsigned)nb), 256, 0, st>>>(bx, d);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+  }
+  return 0;
+}
+
 int row_grid(const lope_layout* L) {
   long long rows = L->padded[1] * L->padded[2];
   long long blocks = (rows * 32 + 255) / 256;
@@ -1912,6 +1984,25 @@ int box_xfer(const lope_layout* layout, void* blk, void* buf, const int64_t* lo,
   return 0;
 }
 }  // namespace
+
+int lope_copy_boxes(const lope_layout* layout, int32_t n, void* const* dst, const void* const* src,
+                    const int64_t* dst_lo, const int64_t* src_lo, const int64_t* extent, void* stream) {
+  if (int e = check_layout(layout)) return e;
+  if (n < 0) return fail(108, "negative box count");
+  if (n == 0) return 0;
+  if (!dst || !src || !dst_lo || !src_lo || !extent) return fail(202, "null argument");
+  for (int32_t i = 0; i < n; ++i) {
+    if (!dst[i] || !src[i]) return fail(202, "box %d has a null buffer", i);
+    for (int d = 0; d < 3; ++d) {
+      const int64_t e = extent[3 * i + d], a = dst_lo[3 * i + d], b = src_lo[3 * i + d];
+      if (e < 0 || a < 0 || b < 0 || a + e > layout->padded[d] || b + e > layout->padded[d])
+        return fail(108, "box %d outside the padded block in dim %d", i, d + 1);
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  return layout->dtype == LOPE_F32 ? copy_boxes_t<float>(layout, n, dst, src, dst_lo, src_lo, extent, st)
+                                   : copy_boxes_t<double>(layout, n, dst, src, dst_lo, src_lo, extent, st);
+}
 
 int lope_box_pack(const lope_layout* layout, const void* blk, const int64_t* lo, const int64_t* extent,
                   void* buf, void* stream) {

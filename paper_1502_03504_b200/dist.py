@@ -665,6 +665,9 @@ class MultiGrid:
                     halo_transfer(b, dims_mask=1 << d)
                 continue
             fb = face_boxes(L, d)
+            # every block's two faces along d in one lope_copy_boxes launch (the halo slabs
+            # written are never read within the same dim)
+            items = []
             for r, b in enumerate(self.blocks):
                 prev = self.blocks[self.grid.neighbour(r, d, -1)]
                 nxt = self.blocks[self.grid.neighbour(r, d, +1)]
@@ -672,10 +675,16 @@ class MultiGrid:
                                                   (fb["high_halo"], nxt, fb["first"])):
                     if dst_box[1][d] == 0:
                         continue
-                    _lib.check(_lib.lib().lope_copy_box(
-                        ctypes.byref(L), ctypes.c_void_p(b.data.data_ptr()), ctypes.c_void_p(src_blk.data.data_ptr()),
-                        (ctypes.c_int64 * 3)(*dst_box[0]), (ctypes.c_int64 * 3)(*src_box[0]),
-                        (ctypes.c_int64 * 3)(*dst_box[1]), _stream_ptr(None)), "lope_copy_box")
+                    items.append((b.data.data_ptr(), src_blk.data.data_ptr(), dst_box[0], src_box[0], dst_box[1]))
+            if items:
+                n = len(items)
+                _lib.check(_lib.lib().lope_copy_boxes(
+                    ctypes.byref(L), n, (ctypes.c_void_p * n)(*[it[0] for it in items]),
+                    (ctypes.c_void_p * n)(*[it[1] for it in items]),
+                    (ctypes.c_int64 * (3 * n))(*[int(v) for it in items for v in it[2]]),
+                    (ctypes.c_int64 * (3 * n))(*[int(v) for it in items for v in it[3]]),
+                    (ctypes.c_int64 * (3 * n))(*[int(v) for it in items for v in it[4]]),
+                    _stream_ptr(None)), "lope_copy_boxes")
 
     def step(self) -> None:
         from .runtime import step

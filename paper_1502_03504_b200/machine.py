@@ -282,17 +282,31 @@ def _make_machine_class():
                     ext[d] = width
                     return lo3, ext
 
+                pending = {}      # destination device -> [(dst ptr, src ptr, dlo, slo, ext)]
+
                 def copy(dst, src, dstart, sstart, width):
-                    # on the destination's GPU; a source on another GPU is read over
-                    # NVLink (peer access enabled at construction)
+                    # queued; flush() issues each phase's slabs as one lope_copy_boxes per
+                    # destination GPU (a source on another GPU is read over NVLink, peer
+                    # access enabled at construction).  Within a phase no slab written
+                    # is read by another, so one launch per phase keeps the semantics.
                     dlo, ext = box(dstart, width)
                     slo, _ = box(sstart, width)
-                    with torch.cuda.device(dst.dev.device):
-                        _lib.check(_lib.lib().lope_copy_box(
-                            ctypes.byref(dst.dev.layout), ctypes.c_void_p(dst.dev.data.data_ptr()),
-                            ctypes.c_void_p(src.dev.data.data_ptr()), (ctypes.c_int64 * 3)(*dlo),
-                            (ctypes.c_int64 * 3)(*slo), (ctypes.c_int64 * 3)(*ext),
-                            ctypes.c_void_p(R._stream_handle())), "lope_copy_box")
+                    pending.setdefault(dst.dev.device, []).append(
+                        (dst.dev.data.data_ptr(), src.dev.data.data_ptr(), dlo, slo, ext))
+
+                def flush():
+                    L = blocks[self.images[0]].dev.layout
+                    for dev, items in pending.items():
+                        n = len(items)
+                        with torch.cuda.device(dev):
+                            _lib.check(_lib.lib().lope_copy_boxes(
+                                ctypes.byref(L), n, (ctypes.c_void_p * n)(*[it[0] for it in items]),
+                                (ctypes.c_void_p * n)(*[it[1] for it in items]),
+                                (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[2]]),
+                                (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[3]]),
+                                (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[4]]),
+                                ctypes.c_void_p(R._stream_handle())), "lope_copy_boxes")
+                    pending.clear()
 
                 low_halo, high_halo = 0, w_lo + m_d
                 low_int, high_int = w_lo, m_d
@@ -309,6 +323,7 @@ def _make_machine_class():
                         self.counters[k]["d2h"] += 1
                         self.events.append(("d2h", k, name, d))
                     blocks[k].state = "device"
+                flush()
                 self._fence()
                 # phase 2: neighbour fills (interior slabs are never written here, so
                 # the image order does not matter)
@@ -322,6 +337,7 @@ def _make_machine_class():
                         copy(blocks[k], blocks[nb], high_halo, low_int, w_hi)
                         self.events.append(("halo_fill", k, name, d, "high"))
                     blocks[k].state = "device"
+                flush()
                 self._fence()
                 # phase 3: push the received halo slabs down to the mirrors
                 for k in self.images:
@@ -336,6 +352,7 @@ def _make_machine_class():
                         self.counters[k]["h2d"] += 1
                         self.events.append(("h2d", k, name, d))
                     mirrors[k].state = "device"
+                flush()
                 self._fence()
 
     return GpuMachine

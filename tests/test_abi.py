@@ -193,6 +193,14 @@ def test_boundary_rejects_bad_calls_with_reference_codes():
     ext = (ctypes.c_int64 * 3)(10, 1, 1)
     assert L.lope_box_pack(ctypes.byref(lay), A, box, ext, B, None) == 108               # box leaves block
     assert L.lope_copy_box(ctypes.byref(lay), A, B, box, box, ext, None) == 108
+    ptrs = (ctypes.c_void_p * 2)(A, B)
+    boxes = (ctypes.c_int64 * 6)(0, 0, 0, 60, 0, 0)
+    exts = (ctypes.c_int64 * 6)(1, 1, 1, 10, 1, 1)
+    assert L.lope_copy_boxes(ctypes.byref(lay), 2, ptrs, ptrs, boxes, boxes, exts, None) == 108   # 2nd box leaves
+    assert L.lope_copy_boxes(ctypes.byref(lay), -1, ptrs, ptrs, boxes, boxes, exts, None) == 108
+    nulls = (ctypes.c_void_p * 2)(A, None)
+    assert L.lope_copy_boxes(ctypes.byref(lay), 2, nulls, ptrs, boxes, boxes, exts, None) == 202
+    assert L.lope_copy_boxes(ctypes.byref(lay), 0, None, None, None, None, None, None) == 0
     assert L.lope_plan_set(h, ctypes.byref(lay), 7, 99, 4, 0) == 108                     # no such variant
     assert L.lope_ipc_close(ctypes.c_void_p(0x1234)) == 108                               # never opened
     # lope_launch bounds-checks every dim before an empty range returns (runtime.py:583-595)

@@ -161,10 +161,11 @@ def run_decomp_case(rng, case):
     lo = [n for n, _ in fp]
     hi = [p for _, p in fp]
     P = rng.choice([2, 3, 4])
+    mx = rng.randrange(9, 60) * vx if rng.random() < 0.5 else rng.randrange(max(lo[0] + hi[0], 5), 200)
     if rank == 2:
-        shape = (rng.randrange(9, 60) * vx, P * rng.randrange(max(lo[1] + hi[1], 3), 20))
+        shape = (mx, P * rng.randrange(max(lo[1] + hi[1], 3), 20))
     else:
-        shape = (rng.randrange(9, 30) * vx, rng.randrange(max(lo[1] + hi[1], 4), 24),
+        shape = (mx, rng.randrange(max(lo[1] + hi[1], 4), 24),
                  P * rng.randrange(max(lo[2] + hi[2], 3), 10))
     if any(s < l + h for s, l, h in zip(shape, lo, hi)):
         return None
