@@ -268,6 +268,8 @@ def _make_machine_class():
             blocks = {k: self._twin(arr, arr.blocks[k], k) for k in self.images}
             mirrors = {k: self._twin(arr, arr.mirrors[k], k) for k in self.images if k in arr.mirrors}
             torch = R._torch()
+            cur_dev = torch.device("cuda", torch.cuda.current_device())
+            cur_stream = ctypes.c_void_p(R._stream_handle())
             self._fence()
             for d in range(rank):
                 w_lo, w_hi = lay.lo[d], lay.hi[d]
@@ -298,14 +300,17 @@ def _make_machine_class():
                     L = blocks[self.images[0]].dev.layout
                     for dev, items in pending.items():
                         n = len(items)
-                        with torch.cuda.device(dev):
-                            _lib.check(_lib.lib().lope_copy_boxes(
-                                ctypes.byref(L), n, (ctypes.c_void_p * n)(*[it[0] for it in items]),
+                        args = (ctypes.byref(L), n, (ctypes.c_void_p * n)(*[it[0] for it in items]),
                                 (ctypes.c_void_p * n)(*[it[1] for it in items]),
                                 (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[2]]),
                                 (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[3]]),
-                                (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[4]]),
-                                ctypes.c_void_p(R._stream_handle())), "lope_copy_boxes")
+                                (ctypes.c_int64 * (3 * n))(*[v for it in items for v in it[4]]))
+                        if dev == cur_dev:      # the common case: no device switch, cached stream
+                            _lib.check(_lib.lib().lope_copy_boxes(*args, cur_stream), "lope_copy_boxes")
+                        else:
+                            with torch.cuda.device(dev):
+                                _lib.check(_lib.lib().lope_copy_boxes(
+                                    *args, ctypes.c_void_p(R._stream_handle())), "lope_copy_boxes")
                     pending.clear()
 
                 low_halo, high_halo = 0, w_lo + m_d

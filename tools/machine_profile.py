@@ -1,5 +1,5 @@
-"""cProfile of the drop-in GPU Machine on config 2's program (4096^2 fp64, 20 steps):
-where the host time of Machine.run() goes.  python tools/machine_profile.py"""
+"""cProfile of the drop-in GPU Machine: where the host time of Machine.run() goes.
+    python tools/machine_profile.py [program] [n] [steps]   (default ninept2d 4096 20)"""
 import cProfile
 import pathlib
 import pstats
@@ -16,14 +16,17 @@ from oracle import lope_oracle as O  # noqa: E402
 from oracle.lope_programs import program_text  # noqa: E402
 from paper_1502_03504_b200.machine import Machine  # noqa: E402
 
-prog, _ = lopec.parse_source(program_text("ninept2d"), "ninept2d.lope")
+name = sys.argv[1] if len(sys.argv) > 1 else "ninept2d"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+prog, _ = lopec.parse_source(program_text(name), f"{name}.lope")
 chk = lopec.check_program(prog)
-field = np.asfortranarray(O.hash_field((4096, 4096), 3, np.float64))
+field = np.asfortranarray(O.hash_field((n, n), 3, np.float64))
 Machine(chk, RunConfig(steps=2), field.copy()).run()
-m = Machine(chk, RunConfig(steps=20), field.copy())
+m = Machine(chk, RunConfig(steps=steps), field.copy())
 pr = cProfile.Profile()
 pr.enable()
 m.run()
 m.gather()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
