@@ -712,7 +712,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-fields", type=int, default=16,
+    ap.add_argument("--e2e-fields", type=int, default=32,
                     help="independent fields in the pipelined e2e batch (1: single calls only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
