@@ -438,9 +438,12 @@ int tiled_smem_bytes(const lope::Kir& k, int dtype, const TileCfg& c) {
   int vx = 16 / sz;
   int bx = 32 * vx * c.bxw, by = c.wy * c.ry;
   int padx = ((k.fn[0][0] + vx - 1) / vx) * vx;
-  int boxx = padx + bx + ((k.fp[0][0] + vx - 1) / vx) * vx;
+  int padr = ((k.fp[0][0] + vx - 1) / vx) * vx;
+  // one TMA box per warp column when a single box would exceed 256 elements
+  const int nb = (padx + bx + padr > 256) ? c.bxw : 1;
+  int boxx = padx + bx / nb + padr;
   int boxy = by + k.fn[0][1] + k.fp[0][1];
-  int stage = ((boxx * boxy * sz + 127) / 128) * 128;
+  int stage = nb * (((boxx * boxy * sz + 127) / 128) * 128);
   if (boxx > 256 || boxy > 256) return 1 << 30;
   return c.ns * stage + 2 * c.ns * 8;
 }

@@ -666,13 +666,20 @@ struct LopeTiledCfg {
   static constexpr int BX = 32 * VX * WX;
   static constexpr int BY = WY * RY;
   static constexpr int PADX = ((Body::FN0 + VX - 1) / VX) * VX;
-  static constexpr int BOXX = PADX + BX + ((Body::FP0 + VX - 1) / VX) * VX;
+  static constexpr int PADR = ((Body::FP0 + VX - 1) / VX) * VX;
+  // A tile wider than one TMA box (256 elements) is staged as one box per warp column
+  // (NB boxes side by side in a stage, each with its own x halo): 256-column fp32 tiles
+  // halve the x-halo sectors per byte that neighbouring tiles must find in L2
+  static constexpr int NB = (PADX + BX + PADR > 256) ? WX : 1;
+  static constexpr int BXB = BX / NB;                  // interior columns per box
+  static constexpr int BOXX = PADX + BXB + PADR;       // row pitch of a staged box
   static constexpr int BOXY = BY + Body::FN1 + Body::FP1;
   static constexpr int NZW = Body::FN2 + Body::FP2 + 1;
   static constexpr bool ZHIST = Body::ZSTAR && Body::FN2 > 0;
   static constexpr int HOLD = ZHIST ? Body::FP2 + 1 : NZW;     // slots one plane iteration holds
-  static constexpr int STAGE_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
-  static constexpr int TX_BYTES = BOXX * BOXY * (int)sizeof(T);
+  static constexpr int BOX_BYTES = ((BOXX * BOXY * (int)sizeof(T) + 127) / 128) * 128;
+  static constexpr int STAGE_BYTES = NB * BOX_BYTES;
+  static constexpr int TX_BYTES = NB * BOXX * BOXY * (int)sizeof(T);
   static constexpr int SMEM_BYTES = NS * STAGE_BYTES + 2 * NS * 8;
   static constexpr int NCW = WX * WY;              // compute warps
   // PW = 1: a dedicated TMA producer warp; PW = 0: warp 0 lane 0 issues TMA in-band
@@ -799,17 +806,22 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
         else if (!lope_mbar_test(&empty[slot], par)) break;
       }
       lope_mbar_expect_tx(&full[slot], C::TX_BYTES);
-      if constexpr (YS) {
-        // rank 2: the unit's planes are consecutive y tiles
-        if (g.p1 > 0)
-          lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + p_pl * C::BY + p_z * g.p1);
-        else
-          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + p_pl * C::BY, p_z);
-      } else {
-        if (g.p1 > 0)
-          lope_tma_load_2d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by + (p_z + p_pl) * g.p1);
-        else
-          lope_tma_load_3d(lope_smem + slot * C::STAGE_BYTES, map, &full[slot], p_bx, p_by, p_z + p_pl);
+#pragma unroll
+      for (int h = 0; h < C::NB; ++h) {
+        unsigned char* dst = lope_smem + slot * C::STAGE_BYTES + h * C::BOX_BYTES;
+        const int bx = p_bx + h * C::BXB;
+        if constexpr (YS) {
+          // rank 2: the unit's planes are consecutive y tiles
+          if (g.p1 > 0)
+            lope_tma_load_2d(dst, map, &full[slot], bx, p_by + p_pl * C::BY + p_z * g.p1);
+          else
+            lope_tma_load_3d(dst, map, &full[slot], bx, p_by + p_pl * C::BY, p_z);
+        } else {
+          if (g.p1 > 0)
+            lope_tma_load_2d(dst, map, &full[slot], bx, p_by + (p_z + p_pl) * g.p1);
+          else
+            lope_tma_load_3d(dst, map, &full[slot], bx, p_by, p_z + p_pl);
+        }
       }
       ++p_L;
       if (++p_pl == p_nl) {
@@ -843,7 +855,9 @@ __device__ __forceinline__ void lope_tiled_impl(const LopeTmap* map, const LopeA
   // The host sends only geometries with ext[0] % VX == 0 and, when images are
   // refreshed, m[0] >= 2*SEC, m[0] % VX == 0 and m[d] >= lo[d] + hi[d] (each halo
   // cell has exactly one image); anything else runs on the generic kernel.
-  const int soff = (row0 * C::BOXX + C::PADX + cx);   // this lane's offset in a stage (elements)
+  // this lane's offset in a stage (elements): its warp column's box, then row and column
+  const int soff = C::NB > 1 ? wx * (C::BOX_BYTES / (int)sizeof(T)) + row0 * C::BOXX + C::PADX + lane * VX
+                             : (row0 * C::BOXX + C::PADX + cx);
 
   LopeUnitWalk w;
   w.init(blockIdx.x, gridDim.x, ntx, yb, nzc);
