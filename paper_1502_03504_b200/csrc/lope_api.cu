@@ -1625,6 +1625,18 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
       t.pw = 1;
       for (int yc : {8, 32}) c.push_back({t, yc, 0});
     }
+    if (K->dtype == LOPE_F64 && base.bxw == 1 && base.wy % 2 == 0) {
+      // wide-footprint fp64 (the 5x5 box): two warp columns x half the warps, dedicated
+      // producer, the deepest ring that fits (config 4 on one box: 2.86-3.02 vs
+      // 3.26-3.40 ms before the power cap, 3.40-3.43 vs 3.45 ms under it;
+      // profiles/r02/s3/wide/s47_*)
+      t = base;
+      t.bxw = 2;
+      t.wy = base.wy / 2;
+      t.pw = 1;
+      while (t.ns > 2 && t.mb * tiled_smem_bytes(K->ir, K->dtype, t) > 225 * 1024) --t.ns;
+      for (int yc : {8, 32}) c.push_back({t, yc, 0});
+    }
   }
   return c;
 }

@@ -276,3 +276,28 @@ def test_run_pinned_batch_fp64_rank2_ragged():
             want = O.periodic_apply(want, kir, None, np.float64)
         got = outs[i].numpy().reshape(shape, order="F")
         assert O.equal_bits(got, want), i
+
+
+@pytest.mark.parametrize("shape", [(512, 70, 19), (301, 45, 13)])
+@pytest.mark.parametrize("tile", [(2, 8, 4, 6, 0, 1, 0, 0), (2, 8, 2, 8, 1, 1, 1, 0)])
+def test_two_box_tiles_match_the_oracle(monkeypatch, shape, tile):
+    """256-column fp32 tiles are staged as one TMA box per warp column (NB = 2): fused
+    steps under such a plan (aligned and ragged x, in-band and dedicated producer) equal
+    the oracle bit for bit."""
+    import ctypes
+    from paper_1502_03504_b200 import _lib
+    monkeypatch.setenv("LOPE_AUTOTUNE", "0")
+    kir = stencils.lap3d7()
+    k = R.CompiledKernel(kir, "float32")
+    lo, hi = [1, 1, 1], [1, 1, 1]
+    field = O.hash_field(shape, 77, np.float32)
+    arr = R.HaloArray(shape, lo, hi, "float32")
+    arr.set_interior(field)
+    _lib.check(_lib.lib().lope_plan_set_variant(k.handle, ctypes.byref(arr.layout), 7, (ctypes.c_int32 * 8)(*tile),
+                                                8, 0, None), "lope_plan_set_variant")
+    R.iterate(k, arr, 4)
+    want = O.machine_run(field, kir, 4, None, np.float32, lo, hi)
+    got = arr.get_padded()
+    assert O.equal_bits(got, want), O.first_mismatch(got, want)
+    n = launches(k)
+    assert n["tiled"] >= 3 and n["generic"] == 0, n
