@@ -435,10 +435,11 @@ def run_gpu_arm(args, wl):
         # replay a recorded plan instead of tuning (profiling captures of one plan)
         import ctypes
         os.environ["LOPE_AUTOTUNE"] = "0"
-        cfg, zc = args.plan.split(":")
+        cfg, zc, *yb = args.plan.split(":")
         vals = [int(v) for v in cfg.split(",")]
         _lib.check(_lib.lib().lope_plan_set_variant(kern.handle, ctypes.byref(arr.layout), (1 << arr.rank) - 1,
-                                                    (ctypes.c_int32 * 8)(*vals), int(zc), 0, None),
+                                                    (ctypes.c_int32 * 8)(*vals), int(zc), int(yb[0]) if yb else 0,
+                                                    None),
                    "lope_plan_set_variant")
     # plan selection (runtime.PlanTuner): real steps under each candidate plan, part
     # of setup like compilation; the timed steps run the chosen plan
@@ -718,7 +719,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--sustained-seconds", type=float, default=1.0)
     ap.add_argument("--plan", default=None,
-                    help="replay a plan 'bxw,wy,ry,ns,pw,mb,sh,nb:zchunk' instead of tuning (ncu captures)")
+                    help="replay a plan 'bxw,wy,ry,ns,pw,mb,sh,nb:zchunk[:yband]' instead of tuning (ncu captures)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")

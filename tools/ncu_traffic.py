@@ -50,9 +50,12 @@ def plan_arg_from_bench(path, workload):
 
 
 def parse_plan(arg):
-    cfg, zc = arg.split(":")
+    cfg, zc, *yb = arg.split(":")
     v = [int(x) for x in cfg.split(",")]
-    return {"tile": v[:4], "producer_warp": v[4], "shfl": v[6], "nb": v[7], "zchunk": int(zc)}
+    d = {"tile": v[:4], "producer_warp": v[4], "shfl": v[6], "nb": v[7], "zchunk": int(zc)}
+    if yb and int(yb[0]):
+        d["yband"] = int(yb[0])
+    return d
 
 
 def main():
@@ -77,12 +80,15 @@ def main():
     ap.add_argument("--skip", type=int, default=8)
     ap.add_argument("--count", type=int, default=5)
     ap.add_argument("--out", default=str(REPO / "gpurun_out"))
+    ap.add_argument("--extra", default="", help="comma-separated further ncu metrics, recorded under 'extra' "
+                    "(L2 sectors and hit rates); the entry is then printed only, not merged")
     a = ap.parse_args()
     plan = a.plan or plan_arg_from_bench(a.from_bench, a.workload)
     out = pathlib.Path(a.out)
     out.mkdir(exist_ok=True)
     log = out / f"ncu_traffic_{a.workload}.csv"
-    cmd = [NCU, "--metrics", "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum",
+    metrics = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum" + (f",{a.extra}" if a.extra else "")
+    cmd = [NCU, "--metrics", metrics,
            "--clock-control", "none", "--cache-control", "none", "-k", f"regex:^{a.kernel}$",
            "--launch-skip", str(a.skip), "-c", str(a.count), "--csv", "--log-file", str(log),
            sys.executable, str(REPO / "bench.py"), "--workload", a.workload, "--plan", plan,
@@ -111,7 +117,10 @@ def main():
              "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                        f"--clock-control none --cache-control none, median of {len(vals['dram__bytes_read.sum'])} "
                        f"{a.kernel} launches after {a.skip}, bench.py --workload {a.workload} --plan {plan}"}
-    merge([entry])
+    if a.extra:
+        entry["extra"] = {m: statistics.median(vals[m]) for m in a.extra.split(",") if m in vals}
+    else:
+        merge([entry])
     print(json.dumps(entry))
 
 
