@@ -612,7 +612,8 @@ def run_gpu_arm(args, wl):
                        "l2": "inputs larger than L2 (no flush needed)" if alg_bytes > 4 * 126e6
                              else "L2-resident working set (config 1); HBM fraction informational",
                        "hbm_gbs_alg": round(alg_bytes * ws / (ms_per_step / 1e3) / 1e9 / ws, 1)},
-            "plan": {"chosen": json.loads(kern.describe()).get("plans"), "tuning_steps": tune_steps,
+            "plan": {"chosen": json.loads(kern.describe()).get("plans"), "timed_window": chosen,
+                     "tuning_steps": tune_steps,
                      "extra_warmup_steps": extra,
                      "watchdog_fallback": [t.report.get("fallback") for t in kern._tuners.values()]},
             "roofline": roofline,

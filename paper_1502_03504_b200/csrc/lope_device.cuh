@@ -396,7 +396,9 @@ __device__ __forceinline__ void lope_mbar_wait(lope_u64* bar, lope_u32 parity) {
         : "r"(addr), "r"(parity)
         : "memory");
 #endif
+#ifndef LOPE_NO_WAIT_TRAP
     if (++n > LOPE_WAIT_LIMIT) __trap();
+#endif
   } while (!done);
 }
 // Non-blocking probe of a barrier phase (mbarrier.test_wait).
