@@ -1378,7 +1378,15 @@ int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n) {
       << "}";
     first = false;
   }
-  o << "},\"launches\":{\"tiled\":" << k->n_tiled.load() << ",\"tiled_multi\":" << k->n_multi.load()
+  // the compiled tile variants (lope_kernel_prepare adds the tuner's candidates)
+  o << "},\"variants\":[";
+  for (size_t i = 0; i < k->variants.size(); ++i) {
+    const TileCfg& c = k->variants[i].tile;
+    o << (i ? "," : "") << "{\"tile\":[" << c.bxw << "," << c.wy << "," << c.ry << "," << c.ns
+      << "],\"producer_warp\":" << c.pw << ",\"shfl\":" << c.sh << ",\"nb\":" << c.nb << ",\"rag\":" << c.rag
+      << ",\"tiled\":" << (k->variants[i].tiled_ok ? "true" : "false") << "}";
+  }
+  o << "],\"launches\":{\"tiled\":" << k->n_tiled.load() << ",\"tiled_multi\":" << k->n_multi.load()
     << ",\"row\":" << k->n_row.load() << ",\"tblock\":" << k->n_tblock.load() << ",\"generic\":"
     << k->n_generic.load() << "}}";
   std::string s = o.str();
@@ -1619,7 +1627,9 @@ std::vector<PlanCand> tune_candidates(const lope_kernel* K) {
     for (int yc : {1, 8, 32}) c.push_back({base, yc, 0});
     TileCfg t = base;
     t.ns = base.ns == 8 ? 12 : 8;
-    for (int yc : {8, 32}) c.push_back({t, yc, 0});
+    while (t.ns > 2 && t.mb * tiled_smem_bytes(K->ir, K->dtype, t) > 225 * 1024) --t.ns;
+    if (t.ns != base.ns)          // (a ring that does not fit shared memory is no candidate)
+      for (int yc : {8, 32}) c.push_back({t, yc, 0});
     if (base.pw == 0) {
       t = base;
       t.pw = 1;

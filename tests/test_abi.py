@@ -81,6 +81,29 @@ def test_kernels_compile_and_describe():
         _lib.destroy_kernel(h)
 
 
+def test_prepared_variants_are_the_tuner_candidates():
+    """lope_kernel_prepare compiles the plan tuner's tile variants (NVRTC, no GPU):
+    every one fits shared memory, the 3-D fp32 list is the six variants behind the
+    nine 3-D plans, and wide-footprint fp64 2-D kernels get the two-warp-column plan."""
+    def variants(name, dt):
+        h = _lib.compile_kernel(serialize(stencils.by_name(name)), dt)
+        try:
+            _lib.check(_lib.lib().lope_kernel_prepare(h), "lope_kernel_prepare")
+            return json.loads(_lib.describe(h))["variants"]
+        finally:
+            _lib.destroy_kernel(h)
+
+    v3 = variants("lap3d7", "f32")
+    assert all(v["tiled"] for v in v3)
+    assert [(v["tile"], v["producer_warp"], v["shfl"], v["nb"]) for v in v3] == [
+        ([1, 16, 2, 8], 0, 0, 0), ([1, 16, 2, 8], 0, 0, 1), ([1, 16, 2, 8], 1, 1, 0),
+        ([1, 16, 2, 10], 1, 1, 0), ([1, 16, 2, 12], 1, 1, 0), ([1, 8, 4, 8], 0, 0, 0)]
+    v5 = variants("box5x5", "f64")
+    assert all(v["tiled"] for v in v5)
+    assert {"tile": [2, 8, 4, 6], "producer_warp": 1, "shfl": 0, "nb": 0, "rag": 0, "tiled": True} in v5
+    assert all(v["tile"][0] == 1 for v in variants("heat2d", "f32"))
+
+
 def test_constants_cross_the_boundary_exactly():
     k = KernelBuilder("c", 2)
     u = k.array("u")
