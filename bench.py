@@ -42,8 +42,8 @@ REPO = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 WORKLOADS = {
-    "c1": dict(kernel="heat2d", shape=(1024, 1024), dtype="float32", split=1,
-               desc="2D 5-point heat 1024x1024 fp32, halo 1 (config 1)"),
+    "c1": dict(kernel="heat2d", shape=(1024, 1024), dtype="float32", split=1, steps=100,
+               desc="2D 5-point heat 1024x1024 fp32, halo 1 (config 1: 100 steps)"),
     "c2": dict(kernel="ninept2d", shape=(16384, 16384), dtype="float32", split=1,
                desc="2D 9-point 16384x16384 fp32, halo 1 (config 2)"),
     "c3": dict(kernel="lap3d7", shape=(1024, 1024, 1024), dtype="float32", split=2,
@@ -709,7 +709,8 @@ def e2e_measure(args, wl, kern, lo, hi, shape, gshape, esz, group, ws, rank, dev
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the configuration's own step count, config 1: 100; else 50)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -725,6 +726,8 @@ def main():
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
     wl = WORKLOADS[args.workload]
+    if args.steps is None:
+        args.steps = wl.get("steps", 50)
     ws_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus != ws_env:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws_env}; launch N>1 with torchrun "

@@ -278,25 +278,35 @@ def test_run_pinned_batch_fp64_rank2_ragged():
         assert O.equal_bits(got, want), i
 
 
-@pytest.mark.parametrize("shape", [(512, 70, 19), (301, 45, 13)])
-@pytest.mark.parametrize("tile", [(2, 8, 4, 6, 0, 1, 0, 0), (2, 8, 2, 8, 1, 1, 1, 0)])
-def test_two_box_tiles_match_the_oracle(monkeypatch, shape, tile):
-    """256-column fp32 tiles are staged as one TMA box per warp column (NB = 2): fused
-    steps under such a plan (aligned and ragged x, in-band and dedicated producer) equal
-    the oracle bit for bit."""
+@pytest.mark.parametrize("name,dt,shape,tile", [
+    ("lap3d7", "float32", (512, 70, 19), (2, 8, 4, 6, 0, 1, 0, 0)),
+    ("lap3d7", "float32", (301, 45, 13), (2, 8, 4, 6, 0, 1, 0, 0)),
+    ("lap3d7", "float32", (512, 70, 19), (2, 8, 2, 8, 1, 1, 1, 0)),
+    ("lap3d7", "float32", (301, 45, 13), (2, 8, 2, 8, 1, 1, 1, 0)),
+    ("box5x5", "float64", (600, 90), (4, 4, 4, 4, 1, 1, 0, 0)),     # 4 boxes of 64+4 columns
+    ("box5x5", "float64", (597, 71), (4, 4, 2, 4, 0, 1, 0, 0)),
+    ("box5x5", "float64", (600, 90), (2, 8, 4, 6, 1, 1, 0, 0)),     # the tuner's two-column plan
+    ("ninept2d", "float32", (1000, 77), (2, 8, 2, 8, 1, 1, 0, 0)),
+])
+def test_two_box_tiles_match_the_oracle(monkeypatch, name, dt, shape, tile):
+    """Tiles wider than one 256-element TMA box are staged as one box per warp column
+    (NB = 2 for 256-column fp32 tiles, 4 for 256-column fp64 tiles): fused steps under
+    such plans (aligned and ragged x, in-band and dedicated producer, rank 2 and 3)
+    equal the oracle bit for bit."""
     import ctypes
     from paper_1502_03504_b200 import _lib
     monkeypatch.setenv("LOPE_AUTOTUNE", "0")
-    kir = stencils.lap3d7()
-    k = R.CompiledKernel(kir, "float32")
-    lo, hi = [1, 1, 1], [1, 1, 1]
-    field = O.hash_field(shape, 77, np.float32)
-    arr = R.HaloArray(shape, lo, hi, "float32")
+    monkeypatch.setenv("LOPE_NO_TBLOCK", "1")
+    kir = stencils.by_name(name)
+    k = R.CompiledKernel(kir, dt)
+    lo, hi = halos(kir)
+    field = O.hash_field(shape, 77, NP[dt])
+    arr = R.HaloArray(shape, lo, hi, dt)
     arr.set_interior(field)
-    _lib.check(_lib.lib().lope_plan_set_variant(k.handle, ctypes.byref(arr.layout), 7, (ctypes.c_int32 * 8)(*tile),
-                                                8, 0, None), "lope_plan_set_variant")
+    _lib.check(_lib.lib().lope_plan_set_variant(k.handle, ctypes.byref(arr.layout), (1 << kir.rank) - 1,
+                                                (ctypes.c_int32 * 8)(*tile), 8, 0, None), "lope_plan_set_variant")
     R.iterate(k, arr, 4)
-    want = O.machine_run(field, kir, 4, None, np.float32, lo, hi)
+    want = O.machine_run(field, kir, 4, None, NP[dt], lo, hi)
     got = arr.get_padded()
     assert O.equal_bits(got, want), O.first_mismatch(got, want)
     n = launches(k)
