@@ -76,7 +76,8 @@ int lope_layout_init(lope_layout* out, int32_t rank, int32_t dtype, const int64_
 /* Compile a kernel from its LOPE1 text (paper_1502_03504_b200/ir.py: serialize). */
 int lope_kernel_compile(const char* ir_text, size_t n, int32_t dtype, lope_kernel** out);
 int lope_kernel_destroy(lope_kernel* k);
-/* JSON description: arrays, scalars, stored arrays, footprints, path chosen. */
+/* JSON description: arrays, scalars, stored arrays, footprints, path chosen, compiled tile
+ * variants, plans per geometry, launches per kernel family. */
 int lope_kernel_describe(const lope_kernel* k, char* buf, size_t n);
 /* Emitted CUDA source of the kernel (for inspection / tests). */
 int lope_kernel_source(const lope_kernel* k, char* buf, size_t n);
