@@ -1369,6 +1369,15 @@ __device__ __forceinline__ void lope_tblock_impl(const LopeArr<T>& a, const Lope
           T* orow = a.out + a.org + (lope_i64)y * a.s1;
           const bool yh = wym && y < g.hi[1], yl = wym && y >= m1 - g.lo[1];
           const lope_i64 yimg = (yh ? (lope_i64)m1 : -(lope_i64)m1) * a.s1;
+          if (!(yh | yl) && x + VX <= m0 && !(wxm && (x < g.hi[0] || x + VX > m0 - g.lo[0]))) {
+            // a whole vector with no periodic image: one 16-byte store
+            V o;
+            T* oe = reinterpret_cast<T*>(&o);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) oe[e] = vals[r][e];
+            *reinterpret_cast<V*>(orow + x) = o;
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < VX; ++e) {
             const int xe = x + e;
