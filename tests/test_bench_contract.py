@@ -45,3 +45,12 @@ def test_reference_arm_port_on_a_3d_config_states_its_sample():
     assert d["e2e"] == {"value": d["value"], "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["gpu_launches"] == 0
+
+
+def test_config1_defaults_to_its_own_step_count():
+    """Without --steps, config 1 is timed over its own 100 steps (BASELINE config 1)."""
+    r = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--workload", "c1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=str(REPO))
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    assert d["steps"] == 100 and d["cpu_baseline"]["steps"] == 100
